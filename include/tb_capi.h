@@ -1,0 +1,155 @@
+/*
+ * tb_capi.h — C ABI of the B200 batched TRON solver (libtronbatch_b200.so).
+ *
+ * This is the drop-in boundary for the reference's solver path.  The
+ * reference (`/root/reference/proj/include/tronbatch/`) is a header-only C++20
+ * library whose API is C++ templates, not an FFI; every entry point below
+ * replaces one reference interface, cited file:line.  The C++ mirror
+ * `include/tronbatch_gpu/solve_batch.hpp` re-exposes exactly the reference
+ * types and signatures on top of this ABI.
+ *
+ * Conventions: plain pointers and sizes only, no CUDA/torch types in the
+ * signatures (streams travel as void*).  Functions return TB_OK or an error
+ * code; tb_last_error() returns a thread-local message.  Batch arrays are
+ * problem-major: x0/lower/upper/x_star are [count][dim], params is
+ * [count][params_stride].
+ */
+#ifndef TB_CAPI_H
+#define TB_CAPI_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- return codes ------------------------------------------------------ */
+#define TB_OK 0
+#define TB_E_INVALID_ARGUMENT 1 /* std::invalid_argument in the reference */
+#define TB_E_CUDA 2
+#define TB_E_NCCL 3
+#define TB_E_PROBLEM 4 /* a problem raised what the reference would throw; see statuses */
+
+/* ---- per-problem status (tron.hpp:83 SolveStatus + extensions) ---------- */
+#define TB_STATUS_CONVERGED 0            /* SolveStatus::Converged */
+#define TB_STATUS_ITER_LIMIT 1           /* SolveStatus::IterLimit */
+#define TB_STATUS_FACTORIZATION_FAILED 2 /* SolveStatus::FactorizationFailed */
+/* extensions: where the reference throws out of solve() (tron.hpp:192,
+ * dense.hpp:222, tron.hpp:170, tron.hpp:466) the device records a status and
+ * the host wrappers rethrow the reference exception type. */
+#define TB_STATUS_EVALUATION_ERROR 3 /* EvaluationError, tron.hpp:192 */
+#define TB_STATUS_ZERO_DIRECTION 4   /* invalid_argument from trqsol, tron.hpp:170 */
+#define TB_STATUS_SINGULAR_FACTOR 5  /* SingularFactorError, dense.hpp:222 */
+#define TB_STATUS_INVALID_BOUNDS 6   /* invalid_argument, tron.hpp:465-466 */
+
+/* ---- problem families (tron.hpp:28-36 BoundedProblem callbacks become
+ *      compile-time device families; see csrc/tb_families.h) ------------- */
+#define TB_FAMILY_HS45 0   /* batch.hpp:116-173 Hs45Problem */
+#define TB_FAMILY_BOXQP 1  /* tests/support/boxqp_oracle.hpp:44-62 make_quadratic */
+#define TB_FAMILY_NCVX 2   /* synthetic nonconvex family */
+#define TB_FAMILY_BRANCH 3 /* ADMM branch subproblem Eq.(3), dim 4 or 6 (line limits) */
+
+#define TB_MEM_HOST 0
+#define TB_MEM_DEVICE 1
+
+#define TB_MODE_EXACT 0 /* reference op order, no FMA: bitwise parity */
+#define TB_MODE_FAST 1  /* FMA contraction + tree reductions (reports flips) */
+
+/* TronConfig (tron.hpp:54-81), field for field; std::optional delta0 becomes
+ * has_delta0 + delta0. */
+typedef struct tb_tron_config {
+    double tol_pg;
+    int32_t has_delta0;
+    double delta0;
+    int32_t max_iter;
+    double cg_tol;
+    double eta0;
+    double sigma1;
+    double sigma2;
+    double sigma3;
+    double mu0;
+    double mu1;
+    double interp_factor;
+    double delta_max;
+} tb_tron_config;
+
+/* std::vector<P> problems + std::vector<Vector> x0s of solve_batch
+ * (batch.hpp:27-29): a family id, the bounds of each problem
+ * (BoundedProblem::lower/upper, tron.hpp:31-32) and its parameters. */
+typedef struct tb_problem_batch {
+    int32_t family;
+    int32_t dim;
+    int64_t count;
+    const double* x0;     /* [count][dim] */
+    const double* lower;  /* [count][dim], -inf allowed (tron.hpp:17) */
+    const double* upper;  /* [count][dim], +inf allowed */
+    const double* params; /* [count][params_stride], may be NULL for HS45 */
+    int64_t params_stride;
+    int32_t memspace; /* TB_MEM_HOST or TB_MEM_DEVICE for all five arrays */
+} tb_problem_batch;
+
+/* BatchResult (batch.hpp:17-22) of SolveReport (tron.hpp:94-103) in SoA
+ * form.  Any per-problem pointer may be NULL to skip that field. */
+typedef struct tb_batch_result {
+    double* x_star;          /* [count][dim] */
+    double* f_star;          /* [count] */
+    double* pg_norm;         /* [count] */
+    int32_t* status;         /* [count] TB_STATUS_* */
+    int32_t* iterations;     /* [count] */
+    int64_t* cg_iterations;  /* [count] (long in the reference) */
+    int64_t* f_evals;        /* [count] */
+    double* wall_time;       /* [count] seconds, per-problem device time (per_problem_time) */
+    int64_t* flops;          /* [count] algorithmic FP64 flops (DESIGN.md model), optional */
+    int32_t memspace;        /* where the per-problem arrays live */
+    /* host-side aggregates, always written */
+    double partition_times[64]; /* seconds per device partition (batch.hpp:20) */
+    int32_t n_partitions;
+    double batch_wall_time; /* seconds (batch.hpp:21) */
+    double kernel_time;     /* seconds, max over devices of the solve kernel */
+} tb_batch_result;
+
+typedef struct tb_context tb_context;
+
+/* TronConfig{} defaults (tron.hpp:55-68). */
+void tb_config_default(tb_tron_config* cfg);
+/* TronConfig::validate (tron.hpp:70-80): TB_OK or TB_E_INVALID_ARGUMENT with
+ * the reference's message in tb_last_error(). */
+int tb_config_validate(const tb_tron_config* cfg);
+
+/* Parameters per problem for (family, dim); -1 if the pair is invalid. */
+int64_t tb_family_nparams(int32_t family, int32_t dim);
+
+/* Device context: one CUDA stream + reusable workspace per device.  The
+ * reference's `workers` argument (batch.hpp:29) becomes the device list: the
+ * batch is split in contiguous even partitions in input order over devices
+ * (batch.hpp:61-70). */
+int tb_context_create(const int32_t* devices, int32_t n_devices, tb_context** out);
+int tb_context_destroy(tb_context* ctx);
+/* TB_MODE_EXACT (default) or TB_MODE_FAST; fast_forward (default 1) skips the
+ * provably identical replays of a rejected zero-change iteration. */
+int tb_context_set_mode(tb_context* ctx, int32_t mode, int32_t fast_forward);
+
+/* solve_batch (batch.hpp:27-78): blocking.  Returns TB_E_PROBLEM if any
+ * problem reports a status >= TB_STATUS_EVALUATION_ERROR (the reference would
+ * have thrown); results are still written. */
+int tb_solve_batch(tb_context* ctx, const tb_problem_batch* batch, const tb_tron_config* cfg,
+                   tb_batch_result* result);
+/* Stream-ordered variant for device-resident batches on a single-device
+ * context: enqueue on `stream` (a cudaStream_t, NULL = the context stream)
+ * and return without synchronising.  Aggregates are not filled. */
+int tb_solve_batch_async(tb_context* ctx, const tb_problem_batch* batch, const tb_tron_config* cfg,
+                         tb_batch_result* result, void* stream);
+
+/* imbalance (batch.hpp:89-111): times is [n_iters][n_parts] row-major. */
+int tb_imbalance(const double* times, int32_t n_iters, int32_t n_parts, double* nu_per_iter,
+                 double* nu_max, double* nu_min, double* nu_mean);
+
+const char* tb_last_error(void);
+/* Number of solver-kernel launches issued since load (evidence counter). */
+int64_t tb_kernel_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* TB_CAPI_H */
