@@ -1,0 +1,466 @@
+// capi.cu — the C ABI (include/tb_capi.h) over the device TRON kernels.
+//
+// solve_batch (batch.hpp:27-78) semantics: validate the config, split the
+// batch into contiguous even partitions in input order (batch.hpp:61-70),
+// one partition per device, solve each on its own stream, and surface the
+// first (in input order) problem that the reference would have thrown on.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/tb_capi.h"
+#include "tb_families.h"
+#include "tron_device.cuh"
+#include "tron_launch.h"
+
+namespace {
+
+thread_local std::string g_err;
+long long g_launches = 0;
+
+int set_err(int code, const char* fmt, ...) {
+    char buf[1024];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    g_err = buf;
+    return code;
+}
+
+#define CUDA_TRY(expr)                                                                     \
+    do {                                                                                   \
+        cudaError_t e_ = (expr);                                                           \
+        if (e_ != cudaSuccess)                                                             \
+            return set_err(TB_E_CUDA, "%s failed: %s", #expr, cudaGetErrorString(e_));     \
+    } while (0)
+
+// device buffer that only grows
+struct DevBuf {
+    void* p = nullptr;
+    size_t cap = 0;
+    cudaError_t ensure(size_t bytes) {
+        if (bytes <= cap) return cudaSuccess;
+        if (p) cudaFree(p);
+        p = nullptr;
+        cap = 0;
+        cudaError_t e = cudaMalloc(&p, bytes);
+        if (e == cudaSuccess) cap = bytes;
+        return e;
+    }
+    void release() {
+        if (p) cudaFree(p);
+        p = nullptr;
+        cap = 0;
+    }
+};
+
+struct DevState {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+    DevBuf in;   // x0, lower, upper, params
+    DevBuf out;  // results
+    DevBuf flag;
+};
+
+__global__ void first_error_kernel(const int32_t* status, long long count, unsigned long long* out) {
+    const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    if (i < count && status[i] >= TB_STATUS_EVALUATION_ERROR) atomicMin(out, (unsigned long long)i);
+}
+
+}  // namespace
+
+struct tb_context {
+    std::vector<DevState> devs;
+    int mode = TB_MODE_EXACT;
+    int fast_forward = 1;
+};
+
+extern "C" {
+
+const char* tb_last_error(void) { return g_err.c_str(); }
+int64_t tb_kernel_launch_count(void) { return g_launches; }
+
+void tb_config_default(tb_tron_config* c) {
+    std::memset(c, 0, sizeof(*c));
+    c->tol_pg = 1e-6;
+    c->max_iter = 200;
+    c->cg_tol = 0.1;
+    c->eta0 = 1e-4;
+    c->sigma1 = 0.25;
+    c->sigma2 = 0.5;
+    c->sigma3 = 4.0;
+    c->mu0 = 1e-2;
+    c->mu1 = 1.0;
+    c->interp_factor = 0.5;
+    c->delta_max = 1e10;
+}
+
+// tron.hpp:70-80, same checks and messages
+int tb_config_validate(const tb_tron_config* c) {
+    if (!c) return set_err(TB_E_INVALID_ARGUMENT, "TronConfig: null");
+    if (!(c->tol_pg > 0.0)) return set_err(TB_E_INVALID_ARGUMENT, "TronConfig: tol_pg must be > 0");
+    if (c->has_delta0 && !(c->delta0 > 0.0))
+        return set_err(TB_E_INVALID_ARGUMENT, "TronConfig: delta0 must be > 0");
+    if (!(0.0 < c->sigma1 && c->sigma1 < c->sigma2 && c->sigma2 < 1.0 && 1.0 < c->sigma3))
+        return set_err(TB_E_INVALID_ARGUMENT, "TronConfig: need 0 < sigma1 < sigma2 < 1 < sigma3");
+    if (!(0.0 < c->eta0 && c->eta0 < 1.0)) return set_err(TB_E_INVALID_ARGUMENT, "TronConfig: need 0 < eta0 < 1");
+    if (!(0.0 < c->mu0 && c->mu0 < 1.0)) return set_err(TB_E_INVALID_ARGUMENT, "TronConfig: need 0 < mu0 < 1");
+    if (!(0.0 < c->interp_factor && c->interp_factor < 1.0))
+        return set_err(TB_E_INVALID_ARGUMENT, "TronConfig: need 0 < interp_factor < 1");
+    if (c->max_iter < 1) return set_err(TB_E_INVALID_ARGUMENT, "TronConfig: max_iter must be >= 1");
+    return TB_OK;
+}
+
+int64_t tb_family_nparams(int32_t family, int32_t dim) {
+    if (!tb_family_dim_ok(family, dim)) return -1;
+    return tb_fam_nparams(family, dim);
+}
+
+int tb_context_create(const int32_t* devices, int32_t n_devices, tb_context** out) {
+    if (!out) return set_err(TB_E_INVALID_ARGUMENT, "tb_context_create: null out");
+    *out = nullptr;
+    int ndev = 0;
+    CUDA_TRY(cudaGetDeviceCount(&ndev));
+    if (n_devices < 1 || n_devices > 64)
+        return set_err(TB_E_INVALID_ARGUMENT, "solve_batch: workers must be >= 1");
+    tb_context* ctx = new tb_context;
+    int prev = 0;
+    cudaGetDevice(&prev);
+    for (int k = 0; k < n_devices; ++k) {
+        DevState d;
+        d.device = devices ? devices[k] : k;
+        if (d.device < 0 || d.device >= ndev) {
+            delete ctx;
+            return set_err(TB_E_INVALID_ARGUMENT, "tb_context_create: device %d out of range (%d visible)",
+                           d.device, ndev);
+        }
+        cudaSetDevice(d.device);
+        cudaError_t e = cudaStreamCreateWithFlags(&d.stream, cudaStreamNonBlocking);
+        for (int i = 0; i < 4 && e == cudaSuccess; ++i) e = cudaEventCreate(&d.ev[i]);
+        if (e != cudaSuccess) {
+            delete ctx;
+            cudaSetDevice(prev);
+            return set_err(TB_E_CUDA, "tb_context_create: %s", cudaGetErrorString(e));
+        }
+        ctx->devs.push_back(d);
+    }
+    cudaSetDevice(prev);
+    *out = ctx;
+    return TB_OK;
+}
+
+int tb_context_destroy(tb_context* ctx) {
+    if (!ctx) return TB_OK;
+    int prev = 0;
+    cudaGetDevice(&prev);
+    for (auto& d : ctx->devs) {
+        cudaSetDevice(d.device);
+        cudaStreamSynchronize(d.stream);
+        for (auto& e : d.ev)
+            if (e) cudaEventDestroy(e);
+        if (d.stream) cudaStreamDestroy(d.stream);
+        d.in.release();
+        d.out.release();
+        d.flag.release();
+    }
+    cudaSetDevice(prev);
+    delete ctx;
+    return TB_OK;
+}
+
+int tb_context_set_mode(tb_context* ctx, int32_t mode, int32_t fast_forward) {
+    if (!ctx) return set_err(TB_E_INVALID_ARGUMENT, "null context");
+    if (mode != TB_MODE_EXACT)
+        return set_err(TB_E_INVALID_ARGUMENT, "only TB_MODE_EXACT is built in this version");
+    ctx->mode = mode;
+    ctx->fast_forward = fast_forward ? 1 : 0;
+    return TB_OK;
+}
+
+int tb_imbalance(const double* times, int32_t n_iters, int32_t n_parts, double* nu, double* nu_max,
+                 double* nu_min, double* nu_mean) {
+    // batch.hpp:89-111
+    if (n_iters < 1) return set_err(TB_E_INVALID_ARGUMENT, "imbalance: need at least one iteration");
+    if (n_parts < 2) return set_err(TB_E_INVALID_ARGUMENT, "imbalance: need at least 2 partitions");
+    for (int k = 0; k < n_iters; ++k) {
+        double tmax = 0.0, tsum = 0.0;
+        for (int p = 0; p < n_parts; ++p) {
+            const double t = times[(long)k * n_parts + p];
+            if (!(t > 0.0)) return set_err(TB_E_INVALID_ARGUMENT, "imbalance: partition times must be positive");
+            tmax = std::max(tmax, t);
+            tsum += t;
+        }
+        const double tmean = tsum / static_cast<double>(n_parts);
+        nu[k] = (tmax / tmean - 1.0) * 100.0;
+    }
+    *nu_max = *std::max_element(nu, nu + n_iters);
+    *nu_min = *std::min_element(nu, nu + n_iters);
+    double s = 0.0;
+    for (int k = 0; k < n_iters; ++k) s += nu[k];
+    *nu_mean = s / static_cast<double>(n_iters);
+    return TB_OK;
+}
+
+}  // extern "C"
+
+namespace {
+
+int check_batch(const tb_problem_batch* b, int64_t* nparams) {
+    if (!b) return set_err(TB_E_INVALID_ARGUMENT, "solve_batch: null batch");
+    if (b->count < 0) return set_err(TB_E_INVALID_ARGUMENT, "solve_batch: negative count");
+    if (b->family < 0 || b->family >= TB_NUM_FAMILIES)
+        return set_err(TB_E_INVALID_ARGUMENT, "solve_batch: unknown problem family %d", b->family);
+    if (!tb_family_dim_ok(b->family, b->dim))
+        return set_err(TB_E_INVALID_ARGUMENT, "solve_batch: dimension %d invalid for family %d", b->dim, b->family);
+    if (b->dim > tbdev::max_warp_dim())
+        return set_err(TB_E_INVALID_ARGUMENT, "solve_batch: dimension %d exceeds device capacity %d", b->dim,
+                       tbdev::max_warp_dim());
+    *nparams = tb_fam_nparams(b->family, b->dim);
+    if (b->count > 0) {
+        if (!b->x0 || !b->lower || !b->upper)
+            return set_err(TB_E_INVALID_ARGUMENT, "solve_batch: null x0/lower/upper");
+        if (*nparams > 0 && (!b->params || b->params_stride < *nparams))
+            return set_err(TB_E_INVALID_ARGUMENT, "solve_batch: params missing or stride %lld < %lld",
+                           (long long)b->params_stride, (long long)*nparams);
+    }
+    if (b->memspace != TB_MEM_HOST && b->memspace != TB_MEM_DEVICE)
+        return set_err(TB_E_INVALID_ARGUMENT, "solve_batch: bad memspace");
+    return TB_OK;
+}
+
+struct OutPtrs {
+    double *x_star, *f_star, *pg;
+    int32_t *status, *iters;
+    int64_t *cg, *fev, *flops;
+    double* wall;
+};
+
+// carve result arrays for `cnt` problems of dim n out of one device buffer
+size_t out_bytes(int64_t cnt, int n) {
+    return (size_t)cnt * (sizeof(double) * (n + 3) + sizeof(int32_t) * 2 + sizeof(int64_t) * 3) + 256;
+}
+OutPtrs carve(void* base, int64_t cnt, int n) {
+    char* p = static_cast<char*>(base);
+    OutPtrs o;
+    o.x_star = reinterpret_cast<double*>(p); p += sizeof(double) * cnt * n;
+    o.f_star = reinterpret_cast<double*>(p); p += sizeof(double) * cnt;
+    o.pg = reinterpret_cast<double*>(p); p += sizeof(double) * cnt;
+    o.wall = reinterpret_cast<double*>(p); p += sizeof(double) * cnt;
+    o.cg = reinterpret_cast<int64_t*>(p); p += sizeof(int64_t) * cnt;
+    o.fev = reinterpret_cast<int64_t*>(p); p += sizeof(int64_t) * cnt;
+    o.flops = reinterpret_cast<int64_t*>(p); p += sizeof(int64_t) * cnt;
+    o.status = reinterpret_cast<int32_t*>(p); p += sizeof(int32_t) * cnt;
+    o.iters = reinterpret_cast<int32_t*>(p);
+    return o;
+}
+
+const char* status_message(int st) {
+    switch (st) {
+        case TB_STATUS_EVALUATION_ERROR: return "EvaluationError: cauchy: non-finite quadratic model value";
+        case TB_STATUS_ZERO_DIRECTION: return "invalid_argument: trqsol: direction is zero, no intersection";
+        case TB_STATUS_SINGULAR_FACTOR: return "SingularFactorError: trtrs: zero diagonal";
+        case TB_STATUS_INVALID_BOUNDS: return "invalid_argument: solve: lower bound exceeds upper bound";
+    }
+    return "unknown";
+}
+
+tbdev::KernelArgs make_args(const tb_problem_batch* b, int64_t np, const tb_tron_config* cfg, int ff,
+                            const double* x0, const double* lo, const double* up, const double* prm,
+                            int64_t stride, int64_t cnt, const OutPtrs& o) {
+    tbdev::KernelArgs a;
+    a.n = b->dim;
+    a.nparams = (int)np;
+    a.count = cnt;
+    a.stride = stride;
+    a.x0 = x0;
+    a.lo = lo;
+    a.up = up;
+    a.prm = np > 0 ? prm : nullptr;
+    a.cfg = *cfg;
+    a.fast_forward = ff;
+    a.x_star = o.x_star;
+    a.f_star = o.f_star;
+    a.pg_norm = o.pg;
+    a.status = o.status;
+    a.iterations = o.iters;
+    a.cg_iterations = o.cg;
+    a.f_evals = o.fev;
+    a.wall_time = o.wall;
+    a.flops = o.flops;
+    return a;
+}
+
+}  // namespace
+
+extern "C" int tb_solve_batch_async(tb_context* ctx, const tb_problem_batch* b, const tb_tron_config* cfg,
+                                    tb_batch_result* r, void* stream) {
+    if (!ctx || !r) return set_err(TB_E_INVALID_ARGUMENT, "solve_batch: null context/result");
+    int rc = tb_config_validate(cfg);
+    if (rc) return rc;
+    int64_t np = 0;
+    if ((rc = check_batch(b, &np))) return rc;
+    if (ctx->devs.size() != 1 || b->memspace != TB_MEM_DEVICE || r->memspace != TB_MEM_DEVICE)
+        return set_err(TB_E_INVALID_ARGUMENT, "solve_batch_async: needs a 1-device context and device memory");
+    DevState& d = ctx->devs[0];
+    CUDA_TRY(cudaSetDevice(d.device));
+    cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : d.stream;
+    OutPtrs o{r->x_star, r->f_star, r->pg_norm, r->status, r->iterations, r->cg_iterations, r->f_evals, r->flops,
+              r->wall_time};
+    tbdev::KernelArgs a = make_args(b, np, cfg, ctx->fast_forward, b->x0, b->lower, b->upper, b->params,
+                                    b->params_stride, b->count, o);
+    CUDA_TRY(tbdev::launch_tron(b->family, a, st));
+    if (b->count > 0) ++g_launches;
+    return TB_OK;
+}
+
+extern "C" int tb_solve_batch(tb_context* ctx, const tb_problem_batch* b, const tb_tron_config* cfg,
+                              tb_batch_result* r) {
+    using clock = std::chrono::steady_clock;
+    if (!ctx || !r) return set_err(TB_E_INVALID_ARGUMENT, "solve_batch: null context/result");
+    int rc = tb_config_validate(cfg);
+    if (rc) return rc;
+    int64_t np = 0;
+    if ((rc = check_batch(b, &np))) return rc;
+    const int G = (int)ctx->devs.size();
+    if ((b->memspace == TB_MEM_DEVICE || r->memspace == TB_MEM_DEVICE) && G != 1)
+        return set_err(TB_E_INVALID_ARGUMENT, "solve_batch: device-resident buffers need a 1-device context");
+    const int n = b->dim;
+    const int64_t N = b->count;
+    const int64_t stride = np > 0 ? b->params_stride : 0;
+    const bool in_host = b->memspace == TB_MEM_HOST;
+    const bool out_host = r->memspace == TB_MEM_HOST;
+    int prev = 0;
+    cudaGetDevice(&prev);
+    const auto t0 = clock::now();
+
+    r->n_partitions = G;
+    std::vector<int64_t> lo(G), cnt(G);
+    {
+        const int64_t base = N / G, rem = N % G;  // batch.hpp:61-70
+        int64_t s = 0;
+        for (int k = 0; k < G; ++k) {
+            lo[k] = s;
+            cnt[k] = base + (k < rem ? 1 : 0);
+            s += cnt[k];
+        }
+    }
+
+    for (int k = 0; k < G; ++k) {
+        DevState& d = ctx->devs[k];
+        CUDA_TRY(cudaSetDevice(d.device));
+        const int64_t c = cnt[k];
+        CUDA_TRY(cudaEventRecord(d.ev[0], d.stream));
+        const double *x0 = b->x0 + lo[k] * n, *lw = b->lower + lo[k] * n, *up = b->upper + lo[k] * n;
+        const double* prm = np > 0 ? b->params + lo[k] * stride : nullptr;
+        if (in_host && c > 0) {
+            const size_t vb = sizeof(double) * (size_t)c * n;
+            const size_t pb = sizeof(double) * (size_t)c * stride;
+            CUDA_TRY(d.in.ensure(3 * vb + pb + 64));
+            char* p = static_cast<char*>(d.in.p);
+            CUDA_TRY(cudaMemcpyAsync(p, x0, vb, cudaMemcpyHostToDevice, d.stream));
+            CUDA_TRY(cudaMemcpyAsync(p + vb, lw, vb, cudaMemcpyHostToDevice, d.stream));
+            CUDA_TRY(cudaMemcpyAsync(p + 2 * vb, up, vb, cudaMemcpyHostToDevice, d.stream));
+            if (pb) CUDA_TRY(cudaMemcpyAsync(p + 3 * vb, prm, pb, cudaMemcpyHostToDevice, d.stream));
+            x0 = reinterpret_cast<const double*>(p);
+            lw = reinterpret_cast<const double*>(p + vb);
+            up = reinterpret_cast<const double*>(p + 2 * vb);
+            prm = pb ? reinterpret_cast<const double*>(p + 3 * vb) : nullptr;
+        }
+        OutPtrs o;
+        if (out_host) {
+            CUDA_TRY(d.out.ensure(out_bytes(c, n)));
+            o = carve(d.out.p, c, n);
+        } else {
+            o = OutPtrs{r->x_star, r->f_star, r->pg_norm, r->status, r->iterations, r->cg_iterations,
+                        r->f_evals, r->flops, r->wall_time};
+            // status is needed for the error scan even if the caller skips it
+            if (!o.status) {
+                CUDA_TRY(d.out.ensure(out_bytes(c, n)));
+                o.status = carve(d.out.p, c, n).status;
+            }
+        }
+        tbdev::KernelArgs a = make_args(b, np, cfg, ctx->fast_forward, x0, lw, up, prm, stride, c, o);
+        CUDA_TRY(cudaEventRecord(d.ev[1], d.stream));
+        CUDA_TRY(tbdev::launch_tron(b->family, a, d.stream));
+        if (c > 0) ++g_launches;
+        CUDA_TRY(cudaEventRecord(d.ev[2], d.stream));
+        if (out_host && c > 0) {
+            auto cp = [&](void* dst, const void* src, size_t bytes) -> cudaError_t {
+                if (!dst) return cudaSuccess;
+                return cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, d.stream);
+            };
+            CUDA_TRY(cp(r->x_star ? r->x_star + lo[k] * n : nullptr, o.x_star, sizeof(double) * c * n));
+            CUDA_TRY(cp(r->f_star ? r->f_star + lo[k] : nullptr, o.f_star, sizeof(double) * c));
+            CUDA_TRY(cp(r->pg_norm ? r->pg_norm + lo[k] : nullptr, o.pg, sizeof(double) * c));
+            CUDA_TRY(cp(r->status ? r->status + lo[k] : nullptr, o.status, sizeof(int32_t) * c));
+            CUDA_TRY(cp(r->iterations ? r->iterations + lo[k] : nullptr, o.iters, sizeof(int32_t) * c));
+            CUDA_TRY(cp(r->cg_iterations ? r->cg_iterations + lo[k] : nullptr, o.cg, sizeof(int64_t) * c));
+            CUDA_TRY(cp(r->f_evals ? r->f_evals + lo[k] : nullptr, o.fev, sizeof(int64_t) * c));
+            CUDA_TRY(cp(r->flops ? r->flops + lo[k] : nullptr, o.flops, sizeof(int64_t) * c));
+            CUDA_TRY(cp(r->wall_time ? r->wall_time + lo[k] : nullptr, o.wall, sizeof(double) * c));
+        }
+        CUDA_TRY(cudaEventRecord(d.ev[3], d.stream));
+    }
+
+    double kmax = 0.0;
+    for (int k = 0; k < G; ++k) {
+        DevState& d = ctx->devs[k];
+        CUDA_TRY(cudaSetDevice(d.device));
+        CUDA_TRY(cudaStreamSynchronize(d.stream));
+        float ms_part = 0.f, ms_kern = 0.f;
+        CUDA_TRY(cudaEventElapsedTime(&ms_part, d.ev[0], d.ev[3]));
+        CUDA_TRY(cudaEventElapsedTime(&ms_kern, d.ev[1], d.ev[2]));
+        if (k < 64) r->partition_times[k] = 1e-3 * ms_part;
+        kmax = std::max(kmax, 1e-3 * (double)ms_kern);
+    }
+    r->kernel_time = kmax;
+    r->batch_wall_time = std::chrono::duration<double>(clock::now() - t0).count();
+
+    // batch.hpp:75-76: the first problem (input order) the reference would
+    // have thrown on turns the whole call into an error.
+    int64_t first_bad = -1;
+    int bad_status = 0;
+    for (int k = 0; k < G && first_bad < 0; ++k) {
+        const int64_t c = cnt[k];
+        if (c == 0) continue;
+        DevState& d = ctx->devs[k];
+        cudaSetDevice(d.device);
+        const int32_t* st_dev = nullptr;
+        if (out_host && r->status) {
+            for (int64_t i = 0; i < c; ++i)
+                if (r->status[lo[k] + i] >= TB_STATUS_EVALUATION_ERROR) {
+                    first_bad = lo[k] + i;
+                    bad_status = r->status[lo[k] + i];
+                    break;
+                }
+            continue;
+        }
+        st_dev = out_host ? carve(d.out.p, c, n).status : (r->status ? r->status : carve(d.out.p, c, n).status);
+        CUDA_TRY(d.flag.ensure(sizeof(unsigned long long)));
+        const unsigned long long init = ~0ull;
+        CUDA_TRY(cudaMemcpyAsync(d.flag.p, &init, sizeof init, cudaMemcpyHostToDevice, d.stream));
+        first_error_kernel<<<(unsigned)((c + 255) / 256), 256, 0, d.stream>>>(
+            st_dev, c, static_cast<unsigned long long*>(d.flag.p));
+        unsigned long long idx = ~0ull;
+        CUDA_TRY(cudaMemcpyAsync(&idx, d.flag.p, sizeof idx, cudaMemcpyDeviceToHost, d.stream));
+        CUDA_TRY(cudaStreamSynchronize(d.stream));
+        if (idx != ~0ull) {
+            int32_t s = 0;
+            CUDA_TRY(cudaMemcpy(&s, st_dev + idx, sizeof s, cudaMemcpyDeviceToHost));
+            first_bad = lo[k] + (int64_t)idx;
+            bad_status = s;
+        }
+    }
+    cudaSetDevice(prev);
+    if (first_bad >= 0)
+        return set_err(TB_E_PROBLEM, "problem %lld: %s", (long long)first_bad, status_message(bad_status));
+    return TB_OK;
+}

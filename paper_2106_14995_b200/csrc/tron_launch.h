@@ -1,0 +1,9 @@
+// tron_launch.h — internal interface between the C ABI layer and the kernels.
+#pragma once
+#include <cuda_runtime.h>
+
+namespace tbdev {
+struct KernelArgs;
+cudaError_t launch_tron(int family, const KernelArgs& a, cudaStream_t st);
+int max_warp_dim();
+}  // namespace tbdev
