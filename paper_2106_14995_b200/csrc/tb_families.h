@@ -188,111 +188,122 @@ TB_HD double tb_ncvx_hess(const double* x, const double* prm, int n, int i, int 
 }
 
 /* ---------------------------------------------------------------- BRANCH */
-/* Per-evaluation shared subexpressions of Eq. (3): flows, their gradients
- * w.r.t. z = (v_i, v_j, th_i, th_j), and the multiplier-like coefficients
- * lambda + rho * residual.  Flows:
+/* Eq. (3) over z = (v_i, v_j, th_i, th_j) [+ slacks (s_ij, s_ji) at dim 6].
+ * Flows, w_i = v_i^2,
+ * wR = v_i v_j cos(th_i - th_j), wI = v_i v_j sin(th_i - th_j):
  *   p_ij =  gff w_i + gft wR + bft wI      q_ij = -bff w_i - bft wR + gft wI
  *   p_ji =  gtt w_j + gtf wR - btf wI      q_ji = -btt w_j - btf wR - gtf wI
- * with w_i = v_i^2, wR = v_i v_j cos(th_i - th_j), wI = v_i v_j sin(...). */
+ * Objective: sum_F lam_F r_F + rho_F/2 r_F^2 (r_F = F - F~) over the four
+ * flows, + the same for w_l = v_l^2 and th_l (l = i, j); dim 6 adds, per line
+ * end, mu h + xi/2 h^2 with h = p^2 + q^2 + s.
+ *
+ * Everything an evaluation point needs is a "context" of independent pieces
+ * (base terms, one block per flow, per voltage coupling, per line end, and
+ * the 4x4 second-derivative tables of wR / wI).  Each piece has one function
+ * used by both the host twin (sequentially) and the device (one lane per
+ * piece, context in shared memory), so both produce identical bits. */
 typedef struct {
-    int n;
-    double vi, vj, cs, sn, wR, wI, wi, wj;
-    double fa[4], fb[4], fc[4]; /* F = fa*w_own + fb*wR + fc*wI */
+    double base[8]; /* vi, vj, cs, sn, wR, wI, wi, wj */
     double F[4];
     double dF[4][4];
-    double cF[4];              /* lam + rho * (F - F~) */
-    double rw[2], cw[2];       /* w residual, lam_w + rho_w * rw */
-    double rt[2], ct[2];       /* theta residual, lam_t + rho_t * rt */
-    double h[2], ch[2];        /* line limit: h = p^2 + q^2 + s, mu + xi h */
+    double cF[4];   /* lam + rho * (F - F~) */
+    double rw[2], cw[2], rt[2], ct[2];
+    double h[2], ch[2];
     double dh[2][4];
+    double d2wR[16], d2wI[16]; /* symmetric 4x4, [a*4 + b] */
 } tb_branch_ctx;
 
-TB_HD void tb_branch_ctx_init(const double* x, const double* prm, int n, tb_branch_ctx* c) {
-    c->n = n;
+enum { TB_BRB_VI, TB_BRB_VJ, TB_BRB_CS, TB_BRB_SN, TB_BRB_WR, TB_BRB_WI, TB_BRB_WII, TB_BRB_WJJ };
+
+TB_HD void tb_br_base(const double* x, double* b) {
     const double vi = x[0], vj = x[1];
     double sn, cs;
     tb_sincos(x[2] - x[3], &sn, &cs);
     const double vv = vi * vj;
-    c->vi = vi; c->vj = vj; c->cs = cs; c->sn = sn;
-    c->wR = vv * cs;
-    c->wI = vv * sn;
-    c->wi = vi * vi;
-    c->wj = vj * vj;
-    const double gff = prm[TB_BR_GFF], bff = prm[TB_BR_BFF], gft = prm[TB_BR_GFT], bft = prm[TB_BR_BFT];
-    const double gtt = prm[TB_BR_GTT], btt = prm[TB_BR_BTT], gtf = prm[TB_BR_GTF], btf = prm[TB_BR_BTF];
-    c->fa[0] = gff;  c->fb[0] = gft;  c->fc[0] = bft;
-    c->fa[1] = -bff; c->fb[1] = -bft; c->fc[1] = gft;
-    c->fa[2] = gtt;  c->fb[2] = gtf;  c->fc[2] = -btf;
-    c->fa[3] = -btt; c->fb[3] = -btf; c->fc[3] = -gtf;
-    const double dwR[4] = {vj * cs, vi * cs, -c->wI, c->wI};
-    const double dwI[4] = {vj * sn, vi * sn, c->wR, -c->wR};
-    const double dwi[4] = {2.0 * vi, 0.0, 0.0, 0.0};
-    const double dwj[4] = {0.0, 2.0 * vj, 0.0, 0.0};
-    for (int f = 0; f < 4; ++f) {
-        const double own = f < 2 ? c->wi : c->wj;
-        const double* down = f < 2 ? dwi : dwj;
-        c->F[f] = (c->fa[f] * own + c->fb[f] * c->wR) + c->fc[f] * c->wI;
-        for (int k = 0; k < 4; ++k)
-            c->dF[f][k] = (c->fa[f] * down[k] + c->fb[f] * dwR[k]) + c->fc[f] * dwI[k];
-        const double r = c->F[f] - prm[TB_BR_TIL + f];
-        c->cF[f] = prm[TB_BR_LAM + f] + prm[TB_BR_RHO + f] * r;
-    }
-    for (int l = 0; l < 2; ++l) {
-        const double v = l == 0 ? vi : vj;
-        c->rw[l] = v * v - prm[TB_BR_WTIL + l];
-        c->cw[l] = prm[TB_BR_LAMW + l] + prm[TB_BR_RHOW + l] * c->rw[l];
-        c->rt[l] = x[2 + l] - prm[TB_BR_TTIL + l];
-        c->ct[l] = prm[TB_BR_LAMT + l] + prm[TB_BR_RHOT + l] * c->rt[l];
-    }
-    for (int l = 0; l < 2; ++l) {
-        c->h[l] = 0.0; c->ch[l] = 0.0;
-        for (int k = 0; k < 4; ++k) c->dh[l][k] = 0.0;
-    }
-    if (n == 6) {
-        for (int l = 0; l < 2; ++l) {
-            const double p = c->F[2 * l], q = c->F[2 * l + 1];
-            c->h[l] = (p * p + q * q) + x[4 + l];
-            c->ch[l] = prm[TB_BR_MU + l] + prm[TB_BR_XI] * c->h[l];
-            for (int k = 0; k < 4; ++k)
-                c->dh[l][k] = (2.0 * p) * c->dF[2 * l][k] + (2.0 * q) * c->dF[2 * l + 1][k];
-        }
+    b[TB_BRB_VI] = vi;
+    b[TB_BRB_VJ] = vj;
+    b[TB_BRB_CS] = cs;
+    b[TB_BRB_SN] = sn;
+    b[TB_BRB_WR] = vv * cs;
+    b[TB_BRB_WI] = vv * sn;
+    b[TB_BRB_WII] = vi * vi;
+    b[TB_BRB_WJJ] = vj * vj;
+}
+
+/* F = fa * w_own + fb * wR + fc * wI */
+TB_HD void tb_br_coef(int f, const double* prm, double* fa, double* fb, double* fc) {
+    switch (f) {
+        case 0: *fa = prm[TB_BR_GFF];  *fb = prm[TB_BR_GFT];  *fc = prm[TB_BR_BFT];  break;
+        case 1: *fa = -prm[TB_BR_BFF]; *fb = -prm[TB_BR_BFT]; *fc = prm[TB_BR_GFT];  break;
+        case 2: *fa = prm[TB_BR_GTT];  *fb = prm[TB_BR_GTF];  *fc = -prm[TB_BR_BTF]; break;
+        default: *fa = -prm[TB_BR_BTT]; *fb = -prm[TB_BR_BTF]; *fc = -prm[TB_BR_GTF]; break;
     }
 }
 
-/* second derivatives of wR / wI, canonical a <= b < 4 */
-TB_HD double tb_branch_d2wR(const tb_branch_ctx* c, int a, int b) {
-    switch (a * 4 + b) {
-        case 1: return c->cs;               /* (vi, vj) */
-        case 2: return -(c->vj * c->sn);    /* (vi, th_i) */
-        case 3: return c->vj * c->sn;       /* (vi, th_j) */
-        case 6: return -(c->vi * c->sn);    /* (vj, th_i) */
-        case 7: return c->vi * c->sn;       /* (vj, th_j) */
-        case 10: return -c->wR;             /* (th_i, th_i) */
-        case 11: return c->wR;              /* (th_i, th_j) */
-        case 15: return -c->wR;             /* (th_j, th_j) */
-    }
-    return 0.0;
+/* flow f: value, gradient over z, and lam + rho * residual */
+TB_HD void tb_br_flow(int f, const double* b, const double* prm, double* F, double* dF, double* cF) {
+    double fa, fb, fc;
+    tb_br_coef(f, prm, &fa, &fb, &fc);
+    const int own = f < 2 ? 0 : 1;
+    const double vi = b[TB_BRB_VI], vj = b[TB_BRB_VJ], cs = b[TB_BRB_CS], sn = b[TB_BRB_SN];
+    const double wR = b[TB_BRB_WR], wI = b[TB_BRB_WI];
+    const double w_own = own == 0 ? b[TB_BRB_WII] : b[TB_BRB_WJJ];
+    const double dwR[4] = {vj * cs, vi * cs, -wI, wI};
+    const double dwI[4] = {vj * sn, vi * sn, wR, -wR};
+    const double dwo[4] = {own == 0 ? 2.0 * vi : 0.0, own == 1 ? 2.0 * vj : 0.0, 0.0, 0.0};
+    *F = (fa * w_own + fb * wR) + fc * wI;
+    for (int k = 0; k < 4; ++k) dF[k] = (fa * dwo[k] + fb * dwR[k]) + fc * dwI[k];
+    *cF = prm[TB_BR_LAM + f] + prm[TB_BR_RHO + f] * (*F - prm[TB_BR_TIL + f]);
 }
-TB_HD double tb_branch_d2wI(const tb_branch_ctx* c, int a, int b) {
-    switch (a * 4 + b) {
-        case 1: return c->sn;
-        case 2: return c->vj * c->cs;
-        case 3: return -(c->vj * c->cs);
-        case 6: return c->vi * c->cs;
-        case 7: return -(c->vi * c->cs);
-        case 10: return -c->wI;
-        case 11: return c->wI;
-        case 15: return -c->wI;
-    }
-    return 0.0;
+
+/* voltage (w = v^2) and angle couplings of bus end l */
+TB_HD void tb_br_volt(int l, const double* x, const double* prm, double* rw, double* cw, double* rt,
+                      double* ct) {
+    const double v = x[l];
+    *rw = v * v - prm[TB_BR_WTIL + l];
+    *cw = prm[TB_BR_LAMW + l] + prm[TB_BR_RHOW + l] * *rw;
+    *rt = x[2 + l] - prm[TB_BR_TTIL + l];
+    *ct = prm[TB_BR_LAMT + l] + prm[TB_BR_RHOT + l] * *rt;
 }
-TB_HD double tb_branch_d2F(const tb_branch_ctx* c, int f, int a, int b) {
+
+/* line-limit term of end l (dim 6): h = p^2 + q^2 + s */
+TB_HD void tb_br_line(int l, const double* x, const double* prm, double p, double q, const double* dp,
+                      const double* dq, double* h, double* ch, double* dh) {
+    *h = (p * p + q * q) + x[4 + l];
+    *ch = prm[TB_BR_MU + l] + prm[TB_BR_XI] * *h;
+    for (int k = 0; k < 4; ++k) dh[k] = (2.0 * p) * dp[k] + (2.0 * q) * dq[k];
+}
+
+/* second derivatives of wR and wI at (a, b), a, b < 4 (symmetric) */
+TB_HD void tb_br_d2w(int a, int b, const double* bs, double* r, double* i) {
+    const int lo = a < b ? a : b, hi = a < b ? b : a;
+    const double vi = bs[TB_BRB_VI], vj = bs[TB_BRB_VJ], cs = bs[TB_BRB_CS], sn = bs[TB_BRB_SN];
+    const double wR = bs[TB_BRB_WR], wI = bs[TB_BRB_WI];
+    double dr = 0.0, di = 0.0;
+    switch (lo * 4 + hi) {
+        case 1: dr = cs; di = sn; break;                      /* (vi, vj) */
+        case 2: dr = -(vj * sn); di = vj * cs; break;         /* (vi, th_i) */
+        case 3: dr = vj * sn; di = -(vj * cs); break;         /* (vi, th_j) */
+        case 6: dr = -(vi * sn); di = vi * cs; break;         /* (vj, th_i) */
+        case 7: dr = vi * sn; di = -(vi * cs); break;         /* (vj, th_j) */
+        case 10: dr = -wR; di = -wI; break;                   /* (th_i, th_i) */
+        case 11: dr = wR; di = wI; break;                     /* (th_i, th_j) */
+        case 15: dr = -wR; di = -wI; break;                   /* (th_j, th_j) */
+        default: break;
+    }
+    *r = dr;
+    *i = di;
+}
+
+TB_HD double tb_br_d2F(const tb_branch_ctx* c, const double* prm, int f, int a, int b) {
+    double fa, fb, fc;
+    tb_br_coef(f, prm, &fa, &fb, &fc);
     const int own = f < 2 ? 0 : 1;
     const double d2own = (a == own && b == own) ? 2.0 : 0.0;
-    return (c->fa[f] * d2own + c->fb[f] * tb_branch_d2wR(c, a, b)) + c->fc[f] * tb_branch_d2wI(c, a, b);
+    return (fa * d2own + fb * c->d2wR[a * 4 + b]) + fc * c->d2wI[a * 4 + b];
 }
 
-TB_HD double tb_branch_f_ctx(const tb_branch_ctx* c, const double* prm) {
+TB_HD double tb_br_f(const tb_branch_ctx* c, const double* prm, int n) {
     double f = 0.0;
     for (int k = 0; k < 4; ++k) {
         const double r = c->F[k] - prm[TB_BR_TIL + k];
@@ -302,39 +313,39 @@ TB_HD double tb_branch_f_ctx(const tb_branch_ctx* c, const double* prm) {
         f += prm[TB_BR_LAMW + l] * c->rw[l] + (0.5 * prm[TB_BR_RHOW + l]) * (c->rw[l] * c->rw[l]);
     for (int l = 0; l < 2; ++l)
         f += prm[TB_BR_LAMT + l] * c->rt[l] + (0.5 * prm[TB_BR_RHOT + l]) * (c->rt[l] * c->rt[l]);
-    if (c->n == 6)
+    if (n == 6)
         for (int l = 0; l < 2; ++l)
             f += prm[TB_BR_MU + l] * c->h[l] + (0.5 * prm[TB_BR_XI]) * (c->h[l] * c->h[l]);
     return f;
 }
 
-TB_HD double tb_branch_grad_ctx(const tb_branch_ctx* c, int k) {
+TB_HD double tb_br_grad(const tb_branch_ctx* c, int n, int k) {
     if (k >= 4) return c->ch[k - 4];
     double g = 0.0;
     for (int f = 0; f < 4; ++f) g += c->cF[f] * c->dF[f][k];
-    if (k < 2) g += c->cw[k] * (2.0 * (k == 0 ? c->vi : c->vj));
+    if (k < 2) g += c->cw[k] * (2.0 * c->base[k]);
     else g += c->ct[k - 2];
-    if (c->n == 6) g += c->ch[0] * c->dh[0][k] + c->ch[1] * c->dh[1][k];
+    if (n == 6) g += c->ch[0] * c->dh[0][k] + c->ch[1] * c->dh[1][k];
     return g;
 }
 
-TB_HD double tb_branch_hess_ctx(const tb_branch_ctx* c, const double* prm, int i, int j) {
+TB_HD double tb_br_hess(const tb_branch_ctx* c, const double* prm, int n, int i, int j) {
     const int a = i < j ? i : j;
     const int b = i < j ? j : i;
     double h = 0.0;
     if (b < 4) {
         for (int f = 0; f < 4; ++f)
-            h += (prm[TB_BR_RHO + f] * c->dF[f][a]) * c->dF[f][b] + c->cF[f] * tb_branch_d2F(c, f, a, b);
+            h += (prm[TB_BR_RHO + f] * c->dF[f][a]) * c->dF[f][b] + c->cF[f] * tb_br_d2F(c, prm, f, a, b);
         if (a == b) {
             if (a < 2) {
-                const double dv = 2.0 * (a == 0 ? c->vi : c->vj);
+                const double dv = 2.0 * c->base[a];
                 h += (prm[TB_BR_RHOW + a] * dv) * dv + c->cw[a] * 2.0;
             } else {
                 h += prm[TB_BR_RHOT + a - 2];
             }
         }
     }
-    if (c->n == 6) {
+    if (n == 6) {
         const double xi = prm[TB_BR_XI];
         for (int l = 0; l < 2; ++l) {
             const double dha = a < 4 ? c->dh[l][a] : (a == 4 + l ? 1.0 : 0.0);
@@ -342,8 +353,8 @@ TB_HD double tb_branch_hess_ctx(const tb_branch_ctx* c, const double* prm, int i
             double sec = 0.0;
             if (b < 4) {
                 const int fp = 2 * l, fq = 2 * l + 1;
-                sec = 2.0 * (((c->dF[fp][a] * c->dF[fp][b] + c->F[fp] * tb_branch_d2F(c, fp, a, b)) +
-                              c->dF[fq][a] * c->dF[fq][b]) + c->F[fq] * tb_branch_d2F(c, fq, a, b));
+                sec = 2.0 * (((c->dF[fp][a] * c->dF[fp][b] + c->F[fp] * tb_br_d2F(c, prm, fp, a, b)) +
+                              c->dF[fq][a] * c->dF[fq][b]) + c->F[fq] * tb_br_d2F(c, prm, fq, a, b));
             }
             h += (xi * dha) * dhb + c->ch[l] * sec;
         }
@@ -351,10 +362,27 @@ TB_HD double tb_branch_hess_ctx(const tb_branch_ctx* c, const double* prm, int i
     return h;
 }
 
+/* host-order construction of the full context (the device builds the same
+ * pieces in parallel lanes) */
+TB_HD void tb_branch_ctx_init(const double* x, const double* prm, int n, tb_branch_ctx* c) {
+    tb_br_base(x, c->base);
+    for (int f = 0; f < 4; ++f) tb_br_flow(f, c->base, prm, &c->F[f], c->dF[f], &c->cF[f]);
+    for (int l = 0; l < 2; ++l) tb_br_volt(l, x, prm, &c->rw[l], &c->cw[l], &c->rt[l], &c->ct[l]);
+    for (int e = 0; e < 16; ++e) tb_br_d2w(e / 4, e % 4, c->base, &c->d2wR[e], &c->d2wI[e]);
+    for (int l = 0; l < 2; ++l) {
+        c->h[l] = 0.0;
+        c->ch[l] = 0.0;
+        for (int k = 0; k < 4; ++k) c->dh[l][k] = 0.0;
+        if (n == 6)
+            tb_br_line(l, x, prm, c->F[2 * l], c->F[2 * l + 1], c->dF[2 * l], c->dF[2 * l + 1], &c->h[l], &c->ch[l],
+                       c->dh[l]);
+    }
+}
+
 TB_HD double tb_branch_f(const double* x, const double* prm, int n) {
     tb_branch_ctx c;
     tb_branch_ctx_init(x, prm, n, &c);
-    return tb_branch_f_ctx(&c, prm);
+    return tb_br_f(&c, prm, n);
 }
 
 /* ------------------------------------------------------- generic dispatch */
@@ -373,7 +401,7 @@ TB_HD void tb_family_grad(int fam, const double* x, const double* prm, int n, do
     if (fam == TB_FAMILY_BRANCH) {
         tb_branch_ctx c;
         tb_branch_ctx_init(x, prm, n, &c);
-        for (int i = 0; i < n; ++i) g[i] = tb_branch_grad_ctx(&c, i);
+        for (int i = 0; i < n; ++i) g[i] = tb_br_grad(&c, n, i);
         return;
     }
     for (int i = 0; i < n; ++i) {
@@ -389,7 +417,7 @@ TB_HD void tb_family_hess(int fam, const double* x, const double* prm, int n, do
         tb_branch_ctx c;
         tb_branch_ctx_init(x, prm, n, &c);
         for (int j = 0; j < n; ++j)
-            for (int i = 0; i < n; ++i) A[i + (long)j * n] = tb_branch_hess_ctx(&c, prm, i, j);
+            for (int i = 0; i < n; ++i) A[i + (long)j * n] = tb_br_hess(&c, prm, n, i, j);
         return;
     }
     for (int j = 0; j < n; ++j)

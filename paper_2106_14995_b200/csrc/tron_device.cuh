@@ -3,21 +3,20 @@
 // Layout: lane i owns variable i.  Vectors (x, g, l, u, s, w, CG state) live
 // in registers, one element per lane; the Hessian A and the shifted Cholesky
 // factor L live in shared memory, column-major with leading dimension D
-// (lane i reads A[i + j*D]: 32 consecutive doubles, conflict-free).  Every
+// (lane i reads A[i + j*D]: consecutive doubles, conflict-free).  Every
 // scalar of the algorithm (f, delta, alpha, rho, ...) is computed redundantly
 // and identically by all 32 lanes, so control flow is warp-uniform.
 //
 // The free-set sub-systems of subspace_step (tron.hpp:405-411: B = A[F,F],
 // compacted) are NOT compacted: every routine takes a lane mask F and walks
-// the free indices in ascending order, which reproduces the compacted loops
-// operation for operation.
+// the free indices in ascending order (set-bit iteration), which reproduces
+// the compacted loops operation for operation.
 //
-// Exact mode (the default build, nvcc --fmad=false): every reduction whose
-// order matters is summed sequentially in ascending index order exactly like
-// dense.hpp:79-84 (dot) and dense.hpp:230-234 (backward solve); min/max and
-// counting reductions (order-independent for the values they see) use warp
-// shuffles.  Results are bit-identical to the reference compiled with
-// -ffp-contract=off.
+// Exact mode (nvcc --fmad=false): every reduction whose order matters is
+// summed sequentially in ascending index order exactly like dense.hpp:79-84
+// (dot) and dense.hpp:230-234 (backward solve); min/max and counting
+// reductions (order-independent for the values they see) use warp shuffles.
+// Results are bit-identical to the reference compiled with -ffp-contract=off.
 #pragma once
 
 #include <cuda_runtime.h>
@@ -34,60 +33,100 @@ constexpr unsigned FULL = 0xffffffffu;
 
 __device__ __forceinline__ int lane_id() { return threadIdx.x & 31; }
 __device__ __forceinline__ bool in_mask(unsigned m, int i) { return (m >> i) & 1u; }
+__device__ __forceinline__ int low_bit(unsigned m) { return __ffs(m) - 1; }
+__device__ __forceinline__ int high_bit(unsigned m) { return 31 - __clz(m); }
+
+struct KernelArgs {
+    int n;
+    int nparams;
+    long long count;
+    long long stride;
+    const double* x0;
+    const double* lo;
+    const double* up;
+    const double* prm;
+    tb_tron_config cfg;
+    int fast_forward;
+    double* x_star;
+    double* f_star;
+    double* pg_norm;
+    int32_t* status;
+    int32_t* iterations;
+    int64_t* cg_iterations;
+    int64_t* f_evals;
+    double* wall_time;
+    int64_t* flops;
+};
+
+// shared memory per warp (doubles)
+template <int D>
+struct SmemLayout {
+    static constexpr int A = 0;                 // D*D Hessian
+    static constexpr int L = A + D * D;         // D*D factor
+    static constexpr int BUF = L + D * D;       // 2*D ordered-sum staging (double buffered)
+    static constexpr int BB = BUF + 2 * D;      // D backward-solve results / second staging
+    static constexpr int XS = BB + D;           // D point for family evaluations
+    static constexpr int CTX = XS + D;          // family context (branch: sizeof(tb_branch_ctx))
+    static constexpr int CTX_DOUBLES = (int)(sizeof(tb_branch_ctx) / sizeof(double));
+    static constexpr int PRM = CTX + CTX_DOUBLES;  // staged parameters
+    static constexpr int fixed() { return PRM; }
+};
 
 // ---------------------------------------------------------------- per warp
 template <int D>
 struct Warp {
-    // shared-memory work areas (set up by the kernel)
-    double* A;    // D*D Hessian
-    double* L;    // D*D shifted Cholesky factor of A[F,F] (original indexing)
-    double* buf;  // D   staging for ordered sums / broadcasts
-    double* bb;   // D   backward-solve results
-    double* xs;   // D   point staged for family evaluations
+    double* A;
+    double* L;
+    double* buf;  // 2*D
+    double* bb;   // D
+    double* xs;   // D
     const double* prm;
+    const tb_tron_config* cfg;
     int n;
     int lane;
-    unsigned act;      // lanes 0..n-1
-    long long fl;      // algorithmic flop counter (tb_flops.h model)
-    tb_tron_config cfg;
+    int tog;        // ordered-sum buffer toggle (0 or D)
+    unsigned act;   // lanes 0..n-1
+    long long fl;   // algorithmic flop counter (tb_flops.h model)
 
     // ------------------------------------------------ ordered reductions
-    // sum_{j in m, ascending} v_j, starting from 0.0 (dense.hpp:81-83)
+    // sum_{j in m, ascending} v_j, starting from 0.0 (dense.hpp:81-83).
+    // Double-buffered staging: one __syncwarp per sum (the other buffer's
+    // readers are ordered by the previous sum's barrier).
     __device__ __forceinline__ double seq_sum(double v, unsigned m) {
-        if (lane < D) buf[lane] = v;
+        double* b = buf + tog;
+        tog ^= D;
+        if (lane < D) b[lane] = v;
         __syncwarp();
         double s = 0.0;
 #pragma unroll
         for (int j = 0; j < D; ++j)
-            if (in_mask(m, j)) s += buf[j];
-        __syncwarp();
+            if (in_mask(m, j)) s += b[j];
         return s;
     }
-    // three independent ordered sums in one pass (same bits as three calls)
-    __device__ __forceinline__ void seq_sum3(double a, double b, double c, unsigned m, double& sa,
-                                             double& sb, double& sc) {
-        double* b2 = buf + 0;
+    // two/three independent ordered sums (same bits as separate calls)
+    __device__ __forceinline__ void seq_sum2(double a, double c, unsigned m, double& sa, double& sc) {
+        double* b = buf + tog;
+        tog ^= D;
+        double* b2 = bb;
         if (lane < D) {
-            b2[lane] = a;
-            bb[lane] = b;
+            b[lane] = a;
+            b2[lane] = c;
         }
         __syncwarp();
         sa = 0.0;
-        sb = 0.0;
-#pragma unroll
-        for (int j = 0; j < D; ++j)
-            if (in_mask(m, j)) {
-                sa += b2[j];
-                sb += bb[j];
-            }
-        __syncwarp();
-        if (lane < D) b2[lane] = c;
-        __syncwarp();
         sc = 0.0;
 #pragma unroll
         for (int j = 0; j < D; ++j)
-            if (in_mask(m, j)) sc += b2[j];
-        __syncwarp();
+            if (in_mask(m, j)) {
+                sa += b[j];
+                sc += b2[j];
+            }
+        __syncwarp();  // bb is not double buffered
+    }
+    __device__ __forceinline__ void seq_sum3(double a, double c, double e, unsigned m, double& sa, double& sc,
+                                             double& se) {
+        seq_sum2(a, c, m, sa, sc);
+        se = seq_sum(e, m);
     }
     __device__ __forceinline__ double dot(double x, double y, unsigned m) {
         fl += 2 * __popc(m);
@@ -112,29 +151,29 @@ struct Warp {
     // y = A[m,m] x over the lanes in m; dense.hpp:104-112 (alpha=1, beta=0):
     // column sweep j ascending, zero-skip on x_j.
     __device__ __forceinline__ double gemv(double x, unsigned m) {
-        if (lane < D) buf[lane] = x;
+        double* b = buf + tog;
+        tog ^= D;
+        if (lane < D) b[lane] = x;
         __syncwarp();
         const int nm = __popc(m);
         double y = 0.0 * 0.0;
+        int used = 0;
 #pragma unroll
         for (int j = 0; j < D; ++j) {
             if (!in_mask(m, j)) continue;
-            const double xj = 1.0 * buf[j];
+            const double xj = 1.0 * b[j];
             if (xj == 0.0) continue;
             y += xj * A[lane + j * D];
-            fl += 2 * nm;
+            ++used;
         }
-        __syncwarp();
+        fl += 2 * nm * used;
         return y;
     }
 
     // ------------------------------------------------ tron.hpp primitives
-    __device__ __forceinline__ double clip(double x, double l, double u) {
-        return tb_smin(tb_smax(x, l), u);
-    }
+    __device__ __forceinline__ double clip(double x, double l, double u) { return tb_smin(tb_smax(x, l), u); }
     // tron.hpp:129-138
-    __device__ __forceinline__ double gpstep(double x, double alpha, double w, double l, double u,
-                                             unsigned m) {
+    __device__ __forceinline__ double gpstep(double x, double alpha, double w, double l, double u, unsigned m) {
         fl += 2 * __popc(m);
         const double trial = x + alpha * w;
         if (trial < l) return l - x;
@@ -142,8 +181,8 @@ struct Warp {
         return alpha * w;
     }
     // tron.hpp:147-164 (min/max over finite breakpoints are order-free)
-    __device__ __forceinline__ void breakpt(double x, double w, double l, double u, unsigned m,
-                                            int& count, double& bmin, double& bmax) {
+    __device__ __forceinline__ void breakpt(double x, double w, double l, double u, unsigned m, double& bmin,
+                                            double& bmax) {
         fl += 2 * __popc(m);
         double b = 0.0;
         bool has = false;
@@ -152,9 +191,7 @@ struct Warp {
             else if (x > l && w < 0.0) { b = (l - x) / w; has = true; }
             if (has && !isfinite(b)) has = false;
         }
-        const unsigned hm = __ballot_sync(FULL, has);
-        count = __popc(hm);
-        if (count == 0) {
+        if (!__any_sync(FULL, has)) {
             bmin = 0.0;
             bmax = 0.0;
             return;
@@ -162,8 +199,8 @@ struct Warp {
         bmin = wmin(has ? b : CUDART_INF);
         bmax = wmax(has ? b : -CUDART_INF);
     }
-    // tron.hpp:112-121: inf-norm of the projected gradient, NaN ignored by
-    // std::max (so NaN lanes contribute 0)
+    // tron.hpp:112-121: inf-norm of the projected gradient; NaN components are
+    // ignored by std::max, so they contribute 0
     __device__ __forceinline__ double pgnorm(double x, double g, double l, double u) {
         double pg = g;
         if (x <= l) pg = tb_smin(g, 0.0);
@@ -173,8 +210,7 @@ struct Warp {
         return wmax(v);
     }
     // tron.hpp:167-176.  Returns 0 or TB_STATUS_ZERO_DIRECTION.
-    __device__ __forceinline__ int trqsol(double x, double w, double delta, unsigned m,
-                                          double& sigma) {
+    __device__ __forceinline__ int trqsol(double x, double w, double delta, unsigned m, double& sigma) {
         double ptx, ptp, xtx;
         seq_sum3(w * x, w * w, x * x, m, ptx, ptp, xtx);
         fl += 6 * __popc(m) + 8;
@@ -188,8 +224,8 @@ struct Warp {
     // tron.hpp:185-188: q(s) = g's + 0.5 s'As; also returns g's
     __device__ __forceinline__ double quad_model(double g, double s, unsigned m, double& gs) {
         const double as = gemv(s, m);
-        double sas, unused;
-        seq_sum3(g * s, s * as, 0.0, m, gs, sas, unused);
+        double sas;
+        seq_sum2(g * s, s * as, m, gs, sas);
         fl += 4 * __popc(m) + 2;
         return gs + 0.5 * sas;
     }
@@ -199,30 +235,32 @@ struct Warp {
     // test !(pivot > 0), divide by sqrt(pivot).  Lane i keeps L(i,j) of the
     // current column in a register.
     __device__ __forceinline__ bool chol_left(unsigned F, int nf, double shift) {
-        int jpos = 0;
+        const bool inF = in_mask(F, lane);
+        int rem = nf;  // free rows at or below the current column
 #pragma unroll 1
-        for (int j = 0; j < D; ++j) {
-            if (!in_mask(F, j)) continue;
-            const bool row = in_mask(F, lane) && lane >= j;
+        for (unsigned mj = F; mj; mj &= mj - 1) {
+            const int j = low_bit(mj);
+            const bool row = inF && lane >= j;
             double lij = row ? A[lane + j * D] : 0.0;
             if (lane == j) lij += shift;
-            fl += 1;
+            long long cnt = 0;
 #pragma unroll 1
-            for (int k = 0; k < j; ++k) {
-                if (!in_mask(F, k)) continue;
+            for (unsigned mk = F & ((1u << j) - 1u); mk; mk &= mk - 1) {
+                const int k = low_bit(mk);
                 const double ljk = L[j + k * D];
                 if (ljk == 0.0) continue;
                 if (row) lij -= ljk * L[lane + k * D];
-                fl += 2 * (nf - jpos);
+                ++cnt;
             }
+            fl += 1 + 2 * rem * cnt;
             const double pivot = bcast(lij, j);
             if (!(pivot > 0.0)) return false;
             const double d = sqrt(pivot);
             if (lane == j) lij = d;
             else if (row) lij = lij / d;
             if (row) L[lane + j * D] = lij;
-            fl += 1 + (nf - jpos - 1);
-            ++jpos;
+            fl += rem;  // sqrt + (rem - 1) divisions
+            --rem;
             __syncwarp();
         }
         return true;
@@ -234,10 +272,9 @@ struct Warp {
         double dg = inF ? fabs(A[lane + lane * D]) : 0.0;
         if (isnan(dg)) dg = 0.0;
         double ma = 0.0;
-#pragma unroll
-        for (int j = 0; j < D; ++j) {
-            if (!in_mask(F, j)) continue;
-            const double v = fabs(A[lane + j * D]);
+#pragma unroll 1
+        for (unsigned mj = F; mj; mj &= mj - 1) {
+            const double v = fabs(A[lane + low_bit(mj) * D]);
             if (inF && !isnan(v)) ma = fmax(ma, v);
         }
         const double max_diag = wmax(dg);
@@ -259,29 +296,30 @@ struct Warp {
     // dense.hpp:224-228 forward solve L b = rhs on F (column sweep == the
     // reference's ascending row dot-form, element by element)
     __device__ __forceinline__ double trsv_fwd(double b, unsigned F, double ldiag) {
+        const bool inF = in_mask(F, lane);
         double s = b;
 #pragma unroll 1
-        for (int j = 0; j < D; ++j) {
-            if (!in_mask(F, j)) continue;
+        for (unsigned mj = F; mj; mj &= mj - 1) {
+            const int j = low_bit(mj);
             if (lane == j) s = s / ldiag;
             const double bj = bcast(s, j);
-            if (in_mask(F, lane) && lane > j) s -= L[lane + j * D] * bj;
+            if (inF && lane > j) s -= L[lane + j * D] * bj;
         }
         return s;
     }
     // dense.hpp:229-235 backward solve L^T b = rhs on F, exact order: for i
     // descending, s = b_i - sum_{j > i ascending} L(j,i) b_j.
     __device__ __forceinline__ double trsv_bwd(double b, unsigned F) {
-        if (lane < D) buf[lane] = b;
-        __syncwarp();
         double out = b;
 #pragma unroll 1
-        for (int i = D - 1; i >= 0; --i) {
-            if (!in_mask(F, i)) continue;
-            double s = buf[i];
+        for (unsigned mi = F; mi; mi &= ~(1u << high_bit(mi))) {
+            const int i = high_bit(mi);
+            double s = bcast(b, i);
 #pragma unroll 1
-            for (int j = i + 1; j < D; ++j)
-                if (in_mask(F, j)) s -= L[j + i * D] * bb[j];
+            for (unsigned mj = F & ~((2u << i) - 1u); mj; mj &= mj - 1) {
+                const int j = low_bit(mj);
+                s -= L[j + i * D] * bb[j];
+            }
             const double bi = s / L[i + i * D];
             if (lane == i) {
                 out = bi;
@@ -289,20 +327,18 @@ struct Warp {
             }
             __syncwarp();
         }
-        __syncwarp();
         return out;
     }
 
     // ------------------------------------------------ tron.hpp:290-344
     // Steihaug PCG on the free set.  Returns 0 or an error status.
     // cg_status: 0 Converged, 1 Boundary, 2 NegCurve, 3 IterCap
-    __device__ __forceinline__ int precond_cg(unsigned F, int nf, double gfree, double delta,
-                                              double ldiag, double& step, int& cg_status,
-                                              int& iters) {
+    __device__ __forceinline__ int precond_cg(unsigned F, int nf, double gfree, double delta, double ldiag,
+                                              double& step, int& cg_status, int& iters) {
         const long long nf2 = (long long)nf * nf;
         double w = 0.0;
         fl += nf;
-        double bhat = trsv_fwd(gfree * -1.0, F, ldiag);
+        const double bhat = trsv_fwd(gfree * -1.0, F, ldiag);
         fl += nf2;
         const double bnorm = nrm2(bhat, F);
         iters = 0;
@@ -347,7 +383,7 @@ struct Warp {
             fl += 4 * nf;
             const double rtr = dot(r, r, F);
             fl += 2;
-            if (sqrt(rtr) <= cfg.cg_tol * bnorm) {
+            if (sqrt(rtr) <= cfg->cg_tol * bnorm) {
                 cg_status = 0;
                 break;
             }
@@ -363,13 +399,11 @@ struct Warp {
     }
 
     // tron.hpp:354-374 on the free set
-    __device__ __forceinline__ double line_search(double x, double l, double u, double g, double w,
-                                                  unsigned F) {
+    __device__ __forceinline__ double line_search(double x, double l, double u, double g, double w, unsigned F) {
         const double kBetaFloor = 1e-12;
         double beta = 1.0;
-        int bc;
         double bmin, bmax;
-        breakpt(x, w, l, u, F, bc, bmin, bmax);
+        breakpt(x, w, l, u, F, bmin, bmax);
         bool search = true;
 #pragma unroll 1
         while (search && beta > bmin && beta > kBetaFloor) {
@@ -377,8 +411,8 @@ struct Warp {
             double gs;
             const double q = quad_model(g, s, F, gs);
             fl += 2 * __popc(F) + 1;
-            if (q <= cfg.mu0 * gs) search = false;
-            else beta *= cfg.interp_factor;
+            if (q <= cfg->mu0 * gs) search = false;
+            else beta *= cfg->interp_factor;
         }
         if (beta < 1.0 && beta < bmin) beta = bmin;
         fl += 2 * __popc(F);
@@ -386,18 +420,17 @@ struct Warp {
     }
 
     // tron.hpp:201-250.  Returns 0 or TB_STATUS_EVALUATION_ERROR.
-    __device__ __forceinline__ int cauchy(double x, double g, double l, double u, double delta,
-                                          double alpha_start, double& alpha_out, double& s) {
+    __device__ __forceinline__ int cauchy(double x, double g, double l, double u, double delta, double alpha_start,
+                                          double& alpha_out, double& s) {
         const unsigned m = act;
         const int nn = n;
-        const double radius = cfg.mu1 * delta;
-        const double extrap_factor = 1.0 / cfg.interp_factor;
+        const double radius = cfg->mu1 * delta;
+        const double extrap_factor = 1.0 / cfg->interp_factor;
         double alpha = alpha_start;
         const double mg = -1.0 * g;
         fl += nn;
-        int bc;
         double bmin, bmax;
-        breakpt(x, mg, l, u, m, bc, bmin, bmax);
+        breakpt(x, mg, l, u, m, bmin, bmax);
         s = gpstep(x, -alpha, g, l, u, m);
         bool interpolate;
         if (nrm2(s, m) > radius) {
@@ -407,20 +440,20 @@ struct Warp {
             const double q = quad_model(g, s, m, gs);
             if (!isfinite(q)) return TB_STATUS_EVALUATION_ERROR;
             fl += 2 * nn + 1;
-            interpolate = q >= cfg.mu0 * gs;
+            interpolate = q >= cfg->mu0 * gs;
         }
         if (interpolate) {
             bool search = true;
 #pragma unroll 1
             while (search && alpha > 1e-30) {
-                alpha *= cfg.interp_factor;
+                alpha *= cfg->interp_factor;
                 s = gpstep(x, -alpha, g, l, u, m);
                 if (nrm2(s, m) <= radius) {
                     double gs;
                     const double q = quad_model(g, s, m, gs);
                     if (!isfinite(q)) return TB_STATUS_EVALUATION_ERROR;
                     fl += 2 * nn + 1;
-                    search = q >= cfg.mu0 * gs;
+                    search = q >= cfg->mu0 * gs;
                 }
             }
         } else {
@@ -435,7 +468,7 @@ struct Warp {
                     const double q = quad_model(g, s, m, gs);
                     if (!isfinite(q)) return TB_STATUS_EVALUATION_ERROR;
                     fl += 2 * nn + 1;
-                    if (q < cfg.mu0 * gs) alpha_good = alpha;
+                    if (q < cfg->mu0 * gs) alpha_good = alpha;
                     else search = false;
                 } else {
                     search = false;
@@ -450,9 +483,8 @@ struct Warp {
 
     // tron.hpp:394-447.  Returns 0 or an error status (factorization failure
     // is TB_STATUS_FACTORIZATION_FAILED, caught by solve like :499-501).
-    __device__ __forceinline__ int subspace_step(double x0, double g, double l, double u,
-                                                 double delta, double cs, double& xout,
-                                                 double& sout, long long& cg_total) {
+    __device__ __forceinline__ int subspace_step(double x0, double g, double l, double u, double delta, double cs,
+                                                 double& xout, double& sout, long long& cg_total) {
         const int nn = n;
         xout = clip(x0 + 1.0 * cs, l, u);
         fl += 2 * nn;
@@ -489,7 +521,7 @@ struct Warp {
             const double t = w + g;
             const double gfnormf = seq_sum(t * t, F);
             fl += 3 * nf + 2;
-            if (sqrt(gfnormf) <= cfg.cg_tol * gfnorm) break;
+            if (sqrt(gfnormf) <= cfg->cg_tol * gfnorm) break;
             if (cgs == 1 || cgs == 3) break;
         }
         sout = s;
@@ -498,59 +530,116 @@ struct Warp {
 };
 
 // ------------------------------------------------------------ families
-template <int FAM>
-struct Family {
-    // objective at the point staged in xs (all lanes, redundantly)
-    static __device__ __forceinline__ double f(const double* xs, const double* prm, int n) {
-        return tb_family_f(FAM, xs, prm, n);
-    }
-    static __device__ __forceinline__ double grad(const double* xs, const double* prm, int n, int i) {
-        if (FAM == TB_FAMILY_HS45) return tb_hs45_grad_i(xs, n, i);
-        if (FAM == TB_FAMILY_BOXQP) return tb_boxqp_grad_i(xs, prm, n, i);
-        if (FAM == TB_FAMILY_NCVX) return tb_ncvx_grad_i(xs, prm, n, i);
-        tb_branch_ctx c;
-        tb_branch_ctx_init(xs, prm, n, &c);
-        return tb_branch_grad_ctx(&c, i);
-    }
-    // row i of the Hessian into A[i + j*ld]
-    static __device__ __forceinline__ void hess_row(const double* xs, const double* prm, int n, int i,
-                                                    double* A, int ld) {
-        if (FAM == TB_FAMILY_BRANCH) {
-            tb_branch_ctx c;
-            tb_branch_ctx_init(xs, prm, n, &c);
-            for (int j = 0; j < n; ++j) A[i + j * ld] = tb_branch_hess_ctx(&c, prm, i, j);
-            return;
-        }
-        for (int j = 0; j < n; ++j) {
-            double v;
-            if (FAM == TB_FAMILY_HS45) v = tb_hs45_hess(xs, n, i, j);
-            else if (FAM == TB_FAMILY_BOXQP) v = tb_boxqp_hess(prm, n, i, j);
-            else v = tb_ncvx_hess(xs, prm, n, i, j);
-            A[i + j * ld] = v;
-        }
-    }
-};
+// Device evaluation of the families of tb_families.h.  prepare(x) builds the
+// per-point context once (cooperatively across lanes); f / grad / hess at the
+// same point reuse it.  The solver only ever evaluates grad and Hessian at the
+// point of the most recent f evaluation (tron.hpp:474-476, 506, 532, 489),
+// so one context per point suffices.  Each value is produced by the same
+// tb_families.h expression as on the host.
+template <int FAM, int D>
+struct DevFamily {
+    double c0 = 0.0, c1 = 0.0, c2 = 0.0, c3 = 0.0;  // per-lane caches
+    tb_branch_ctx* ctx = nullptr;
 
-struct KernelArgs {
-    int n;
-    int nparams;
-    long long count;
-    long long stride;
-    const double* x0;
-    const double* lo;
-    const double* up;
-    const double* prm;
-    tb_tron_config cfg;
-    int fast_forward;
-    double* x_star;
-    double* f_star;
-    double* pg_norm;
-    int32_t* status;
-    int32_t* iterations;
-    int64_t* cg_iterations;
-    int64_t* f_evals;
-    double* wall_time;
-    int64_t* flops;
+    __device__ __forceinline__ void prepare(Warp<D>& W, double x) {
+        const int lane = W.lane, n = W.n;
+        const bool act = lane < n;
+        if (act) W.xs[lane] = x;
+        __syncwarp();
+        const double* xs = W.xs;
+        const double* prm = W.prm;
+        if (FAM == TB_FAMILY_BOXQP) {
+            if (act) {
+                c0 = x - prm[(long)n * n + lane];    // d_i
+                c1 = tb_boxqp_hd_i(xs, prm, n, lane); // (H d)_i
+            }
+        } else if (FAM == TB_FAMILY_NCVX) {
+            if (act) {
+                const double* c = prm + (long)n * (n + 1) / 2;
+                c0 = x - c[lane];                    // e_i
+                c1 = tb_ncvx_he_i(xs, prm, n, lane);  // (H e)_i
+                tb_sincos(x, &c2, &c3);              // sin, cos
+            }
+        } else if (FAM == TB_FAMILY_BRANCH) {
+            tb_branch_ctx* c = ctx;
+            double b[8];
+            tb_br_base(xs, b);
+            if (lane < 8) c->base[lane] = b[lane];
+            if (lane < 4) tb_br_flow(lane, b, prm, &c->F[lane], c->dF[lane], &c->cF[lane]);
+            else if (lane < 6) {
+                const int l = lane - 4;
+                tb_br_volt(l, xs, prm, &c->rw[l], &c->cw[l], &c->rt[l], &c->ct[l]);
+            }
+            if (lane >= 8 && lane < 24) {
+                const int e = lane - 8;
+                tb_br_d2w(e / 4, e % 4, b, &c->d2wR[e], &c->d2wI[e]);
+            }
+            __syncwarp();
+            if (lane < 2) {
+                const int l = lane;
+                if (n == 6) {
+                    tb_br_line(l, xs, prm, c->F[2 * l], c->F[2 * l + 1], c->dF[2 * l], c->dF[2 * l + 1], &c->h[l],
+                               &c->ch[l], c->dh[l]);
+                } else {
+                    c->h[l] = 0.0;
+                    c->ch[l] = 0.0;
+                    for (int k = 0; k < 4; ++k) c->dh[l][k] = 0.0;
+                }
+            }
+            __syncwarp();
+        }
+    }
+    __device__ __forceinline__ double f(Warp<D>& W) {
+        const int lane = W.lane, n = W.n;
+        const double* prm = W.prm;
+        if (FAM == TB_FAMILY_HS45) return tb_hs45_f(W.xs, n);
+        if (FAM == TB_FAMILY_BOXQP) return 0.5 * W.seq_sum(c0 * c1, W.act);
+        if (FAM == TB_FAMILY_NCVX) {
+            const double* k = prm + (long)n * (n + 1) / 2 + n;
+            const double* a = k + n;
+            const double e2 = c0 * c0;
+            double q, quart, sn;
+            const double kq = lane < n ? k[lane] * (e2 * e2) : 0.0;
+            const double as = lane < n ? a[lane] * c2 : 0.0;
+            W.seq_sum3(c0 * c1, kq, as, W.act, q, quart, sn);
+            return (0.5 * q + 0.25 * quart) + sn;
+        }
+        return tb_br_f(ctx, prm, n);
+    }
+    __device__ __forceinline__ double grad(Warp<D>& W) {
+        const int lane = W.lane, n = W.n;
+        if (lane >= n) return 0.0;
+        const double* prm = W.prm;
+        if (FAM == TB_FAMILY_HS45) return tb_hs45_grad_i(W.xs, n, lane);
+        if (FAM == TB_FAMILY_BOXQP) return c1;
+        if (FAM == TB_FAMILY_NCVX) {
+            const double* k = prm + (long)n * (n + 1) / 2 + n;
+            const double* a = k + n;
+            const double e3 = (c0 * c0) * c0;
+            return (c1 + k[lane] * e3) + a[lane] * c3;
+        }
+        return tb_br_grad(ctx, n, lane);
+    }
+    // row `lane` of the Hessian into A[lane + j*D]
+    __device__ __forceinline__ void hess(Warp<D>& W) {
+        const int lane = W.lane, n = W.n;
+        const double* prm = W.prm;
+        if (lane < n) {
+            if (FAM == TB_FAMILY_HS45) {
+                for (int j = 0; j < n; ++j) W.A[lane + j * D] = tb_hs45_hess(W.xs, n, lane, j);
+            } else if (FAM == TB_FAMILY_BOXQP) {
+                for (int j = 0; j < n; ++j) W.A[lane + j * D] = tb_boxqp_hess(prm, n, lane, j);
+            } else if (FAM == TB_FAMILY_NCVX) {
+                const double* k = prm + (long)n * (n + 1) / 2 + n;
+                const double* a = k + n;
+                for (int j = 0; j < n; ++j) W.A[lane + j * D] = tb_ncvx_H(prm, n, lane, j);
+                W.A[lane + lane * D] = (W.A[lane + lane * D] + (3.0 * k[lane]) * (c0 * c0)) - a[lane] * c2;
+            } else {
+                for (int j = 0; j < n; ++j) W.A[lane + j * D] = tb_br_hess(ctx, prm, n, lane, j);
+            }
+        }
+        __syncwarp();
+    }
 };
 
 __device__ __forceinline__ unsigned long long globaltimer() {
@@ -559,31 +648,28 @@ __device__ __forceinline__ unsigned long long globaltimer() {
     return t;
 }
 
-template <int D>
-constexpr int smem_doubles_fixed() {
-    return 2 * D * D + 3 * D;
-}
-
 // tron.hpp:453-549 solve(), one problem per warp (one warp per block).
 template <int FAM, int D>
-__global__ void __launch_bounds__(32) tron_solve_kernel(const KernelArgs a) {
+__global__ void __launch_bounds__(32, 16) tron_solve_kernel(const __grid_constant__ KernelArgs a) {
     extern __shared__ double smem[];
+    using SL = SmemLayout<D>;
     const long long pid = blockIdx.x;
     if (pid >= a.count) return;
     const unsigned long long t_start = globaltimer();
 
     Warp<D> W;
-    W.A = smem;
-    W.L = smem + D * D;
-    W.buf = smem + 2 * D * D;
-    W.bb = W.buf + D;
-    W.xs = W.bb + D;
-    double* prm_s = W.xs + D;
+    W.A = smem + SL::A;
+    W.L = smem + SL::L;
+    W.buf = smem + SL::BUF;
+    W.bb = smem + SL::BB;
+    W.xs = smem + SL::XS;
+    double* prm_s = smem + SL::PRM;
     W.n = a.n;
     W.lane = lane_id();
+    W.tog = 0;
     W.act = (a.n >= 32) ? FULL : ((1u << a.n) - 1u);
     W.fl = 0;
-    W.cfg = a.cfg;
+    W.cfg = &a.cfg;
     const int n = a.n;
     const int lane = W.lane;
     const bool act = lane < n;
@@ -595,9 +681,12 @@ __global__ void __launch_bounds__(32) tron_solve_kernel(const KernelArgs a) {
         for (int k = lane; k < a.nparams; k += 32) prm_s[k] = gp[k];
     }
     W.prm = prm_s;
+    DevFamily<FAM, D> fam;
+    fam.ctx = reinterpret_cast<tb_branch_ctx*>(smem + SL::CTX);
     const double l = act ? a.lo[pid * n + lane] : 0.0;
     const double u = act ? a.up[pid * n + lane] : 0.0;
     double x = act ? a.x0[pid * n + lane] : 0.0;
+    __syncwarp();
 
     int status = TB_STATUS_ITER_LIMIT;
     int iterations = 0;
@@ -610,14 +699,12 @@ __global__ void __launch_bounds__(32) tron_solve_kernel(const KernelArgs a) {
     } else {
         const double kEta1 = 0.25, kEta2 = 0.75;
         x = W.clip(x, l, u);
-        if (act) W.xs[lane] = x;
-        __syncwarp();
-        f = Family<FAM>::f(W.xs, prm_s, n);
+        fam.prepare(W, x);
+        f = fam.f(W);
         W.fl += tb_family_flops(FAM, n, 0);
         f_evals = 1;
-        double g = act ? Family<FAM>::grad(W.xs, prm_s, n, lane) : 0.0;
+        double g = fam.grad(W);
         W.fl += tb_family_flops(FAM, n, 1);
-        __syncwarp();
         pg = W.pgnorm(x, g, l, u);
         double delta = cfg.has_delta0 ? cfg.delta0 : tb_smax(W.nrm2(g, W.act), 1.0);
         double alpha_c = 1.0;
@@ -628,12 +715,10 @@ __global__ void __launch_bounds__(32) tron_solve_kernel(const KernelArgs a) {
 #pragma unroll 1
             for (int iter = 1; iter <= cfg.max_iter; ++iter) {
                 iterations = iter;
-                if (need_hessian) {
-                    // x is staged in W.xs (at entry or after acceptance)
-                    if (act) Family<FAM>::hess_row(W.xs, prm_s, n, lane, W.A, D);
+                if (need_hessian) {  // family context holds the current x
+                    fam.hess(W);
                     W.fl += tb_family_flops(FAM, n, 2);
                     need_hessian = false;
-                    __syncwarp();
                 }
                 const long long fl_iter0 = W.fl;
                 const double delta_in = delta, alpha_in = alpha_c;
@@ -648,19 +733,13 @@ __global__ void __launch_bounds__(32) tron_solve_kernel(const KernelArgs a) {
                 double xt, s;
                 long long cg_its;
                 rc = W.subspace_step(x, g, l, u, delta, cs, xt, s, cg_its);
-                if (rc == TB_STATUS_FACTORIZATION_FAILED) {
-                    status = TB_STATUS_FACTORIZATION_FAILED;
-                    break;
-                }
                 if (rc) {
-                    status = rc;
+                    status = rc;  // FactorizationFailed caught like tron.hpp:499-501
                     break;
                 }
                 cg_iterations += cg_its;
-                // f at the trial point (stage it; restage x if rejected)
-                if (act) W.xs[lane] = xt;
-                __syncwarp();
-                const double f_trial = Family<FAM>::f(W.xs, prm_s, n);
+                fam.prepare(W, xt);
+                const double f_trial = fam.f(W);
                 W.fl += tb_family_flops(FAM, n, 0);
                 ++f_evals;
 
@@ -691,20 +770,16 @@ __global__ void __launch_bounds__(32) tron_solve_kernel(const KernelArgs a) {
 
                 const bool accepted = actred > cfg.eta0 * prered;
                 if (accepted) {
-                    x = xt;  // W.xs already holds xt
+                    x = xt;
                     f = f_trial;
-                    g = act ? Family<FAM>::grad(W.xs, prm_s, n, lane) : 0.0;
+                    g = fam.grad(W);  // context was prepared at xt
                     W.fl += tb_family_flops(FAM, n, 1);
-                    __syncwarp();
                     need_hessian = true;
                     pg = W.pgnorm(x, g, l, u);
                     if (pg <= cfg.tol_pg) {
                         status = TB_STATUS_CONVERGED;
                         break;
                     }
-                } else {
-                    if (act) W.xs[lane] = x;
-                    __syncwarp();
                 }
                 if (delta <= 1e-300) break;
                 // Zero-change fixed point: a rejected
@@ -712,8 +787,7 @@ __global__ void __launch_bounds__(32) tron_solve_kernel(const KernelArgs a) {
                 // unchanged leaves the whole solver state (x, f, g, A, delta,
                 // alpha_c) unchanged, so every remaining iteration replays it
                 // exactly.  Fast-forward with identical counters.
-                if (a.fast_forward && !accepted && iter >= 2 && delta == delta_in &&
-                    alpha_c == alpha_in) {
+                if (a.fast_forward && !accepted && iter >= 2 && delta == delta_in && alpha_c == alpha_in) {
                     const long long rem = cfg.max_iter - iter;
                     cg_iterations += rem * cg_its;
                     f_evals += rem;

@@ -9,7 +9,7 @@ namespace tbdev {
 template <int FAM, int D>
 static cudaError_t launch_fd(const KernelArgs& a, cudaStream_t st) {
     const int np = (a.nparams + 1) & ~1;
-    const size_t smem = sizeof(double) * (size_t)(smem_doubles_fixed<D>() + np);
+    const size_t smem = sizeof(double) * (size_t)(SmemLayout<D>::fixed() + np);
     auto kern = tron_solve_kernel<FAM, D>;
     if (smem > 48 * 1024) {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
