@@ -1,0 +1,334 @@
+#!/usr/bin/env python
+"""Benchmark of the batched TRON hot path (BASELINE.json configs[1], C2):
+65,536 synthetic AC-OPF branch augmented-Lagrangian subproblems (d = 6) per GPU.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+One step = one batched solve of the whole per-GPU batch (weak scaling: every
+rank solves its own 65,536-problem batch; no collective on the data path).
+Prints ONE JSON line on rank 0.
+
+value : solves/s over all ranks, inputs resident in HBM, device time of the
+        solve kernel (CUDA events on the launching stream, L2 flushed between
+        steps outside the timed events), max over ranks.
+e2e   : same metric through the public API with pinned HOST buffers
+        (H2D of x0/l/u/params + kernel + D2H of every SolveReport field).
+--impl reference : the reference's own CPU solve_batch (the unmodified
+        reference headers compiled into oracle/_ref/libtronref.so, all host
+        threads) on a bounded sample of the same workload; rank 0 only.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+BATCH = 65536
+DIM = 6
+METRIC = "bound-constrained solves/sec (batch, FP64)"
+WORKLOAD = "C2: 65,536 synthetic AC-OPF branch augmented-Lagrangian subproblems (d=6) per GPU"
+
+
+def env_int(k, d):
+    try:
+        return int(os.environ.get(k, d))
+    except ValueError:
+        return d
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.rows = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.Q}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                                     timeout=5).stdout.strip()
+                if out:
+                    self.rows.append([c.strip() for c in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if len(r) > 5 + i and r[5 + i] == "Active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+def cpu_reference_run(batch, workers, reps=1):
+    """The reference's own solve_batch (oracle/_ref) on `batch`; returns
+    (solves/s best of reps, wall seconds)."""
+    from oracle import pyoracle
+
+    best = 0.0
+    total = 0.0
+    for _ in range(reps):
+        t0 = time.perf_counter()
+        r = pyoracle.solve_batch(batch, impl="ref", workers=workers)
+        dt = time.perf_counter() - t0
+        total += dt
+        assert r.rc == 0, f"reference solve_batch threw: {pyoracle.last_error()}"
+        best = max(best, batch.count / r.batch_wall_time)
+    return best, total
+
+
+def cpu_sample(full_batch, seconds_target=1.5, workers=1, rate_guess=15000.0):
+    from paper_2106_14995_b200 import ProblemBatch
+
+    n = int(min(full_batch.count, max(256, seconds_target * rate_guess * workers)))
+    return ProblemBatch(full_batch.family, full_batch.dim, full_batch.lower[:n], full_batch.upper[:n],
+                        full_batch.params[:n], full_batch.x0[:n]), n
+
+
+def run_reference_arm(args, rank, world):
+    if rank != 0:
+        return 0
+    from oracle import pyoracle
+    from paper_2106_14995_b200 import synth
+
+    if not pyoracle.ref_available():
+        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libtronref.so not built (needs /root/reference at build time)"}))
+        return 0
+    cores = os.cpu_count() or 1
+    full = synth.branch(BATCH, DIM, seed=2)
+    sample, n = cpu_sample(full, seconds_target=2.0, workers=cores)
+    for _ in range(max(1, args.warmup)):
+        cpu_reference_run(sample, cores)
+    vals = []
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        v, _ = cpu_reference_run(sample, cores)
+        vals.append(v)
+    wall = time.perf_counter() - t0
+    value = world * statistics.median(vals) if False else statistics.median(vals)
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "solves/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * wall / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": WORKLOAD, "family": "branch", "dim": DIM, "batch": BATCH, "seed": 2},
+        "cpu_baseline": {"value": value, "unit": "solves/s", "cores": cores, "kind": "reference",
+                         "sample": f"first {n} of the {BATCH} C2 problems per step, reference solve_batch(workers={cores})"},
+        "e2e": {"value": value, "unit": "solves/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--batch", type=int, default=BATCH)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(3, args.warmup) if args.impl == "ours" else args.warmup
+
+    rank, world, local = env_int("RANK", 0), env_int("WORLD_SIZE", 1), env_int("LOCAL_RANK", 0)
+    if args.impl == "reference":
+        return run_reference_arm(args, rank, world)
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_2106_14995_b200 import Solver, TronConfig, _lib, synth
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    lib = _lib.load()
+    solver = Solver((local,))
+    cfg = TronConfig()
+    batch = synth.branch(args.batch, DIM, seed=2 + rank)
+    N = batch.count
+
+    # ---- device-resident inputs (HBM) and outputs
+    t = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(dev)  # noqa: E731
+    from paper_2106_14995_b200 import ProblemBatch
+
+    dbatch = ProblemBatch(batch.family, batch.dim, t(batch.lower), t(batch.upper), t(batch.params), t(batch.x0))
+    dout = Solver.alloc_result(N, DIM, device=True)
+    flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)  # > 126 MB L2
+    stream = torch.cuda.current_stream(dev)
+
+    def device_step():
+        solver.solve_batch(dbatch, cfg=cfg, out=dout, stream=stream.cuda_stream)
+
+    for _ in range(args.warmup):
+        device_step()
+    torch.cuda.synchronize(dev)
+
+    # parity spot check (bitwise vs the CPU oracle) on the first 512 problems
+    parity = None
+    if rank == 0:
+        try:
+            from oracle import pyoracle
+
+            m = min(512, N)
+            sub = ProblemBatch(batch.family, DIM, batch.lower[:m], batch.upper[:m], batch.params[:m], batch.x0[:m])
+            ref = pyoracle.solve_batch(sub, impl="oracle", workers=os.cpu_count() or 1)
+            ok = all(np.array_equal(getattr(dout, k)[:m].cpu().numpy(), getattr(ref, k))
+                     for k in ("x_star", "f_star", "pg_norm", "status", "iterations", "cg_iterations", "f_evals"))
+            parity = f"bitwise {'match' if ok else 'MISMATCH'} vs CPU oracle on first {m} problems"
+        except Exception as e:  # oracle not built on this box
+            parity = f"not checked ({e})"
+
+    # ---- timed region: device-resident
+    launches0 = lib.tb_kernel_launch_count()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    barrier()
+    torch.cuda.synchronize(dev)
+    with ClockSampler(local) as clocks:
+        for k in range(args.steps):
+            flush.random_(0, 255)  # untimed L2 flush between steps
+            ev[k][0].record(stream)
+            device_step()
+            ev[k][1].record(stream)
+        torch.cuda.synchronize(dev)
+    barrier()
+    launches = lib.tb_kernel_launch_count() - launches0
+    ms_steps = [a.elapsed_time(b) for a, b in ev]
+    ms_total = sum(ms_steps)
+    mx = torch.tensor([ms_total], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(mx, op=dist.ReduceOp.MAX)
+    ms_total = float(mx.item())
+    ms_per_step = ms_total / args.steps
+    value = world * N / (ms_per_step * 1e-3)
+
+    # ---- algorithmic flops per launch (device counters; deterministic)
+    flops_per_launch = float(dout.flops.sum().item())
+    status = dout.status.cpu().numpy()
+    achieved_tflops = flops_per_launch / (ms_per_step * 1e-3) / 1e12
+    peak = _lib.C.c_double()
+    lib.tb_measure_fp64_peak(local, _lib.C.byref(peak))
+    fp64_peak = peak.value
+
+    # ---- e2e through the public API with pinned host buffers
+    def pinned(a):
+        p = torch.empty(a.shape, dtype=torch.float64, pin_memory=True)
+        p.copy_(torch.from_numpy(np.ascontiguousarray(a)))
+        return p.numpy()
+
+    hbatch = ProblemBatch(batch.family, DIM, pinned(batch.lower), pinned(batch.upper), pinned(batch.params),
+                          pinned(batch.x0))
+    hout = Solver.alloc_result(N, DIM, device=False)
+    for name in ("x_star", "f_star", "pg_norm", "per_problem_time"):
+        a = getattr(hout, name)
+        setattr(hout, name, pinned(np.zeros(a.shape)))
+    for _ in range(2):
+        solver.solve_batch(hbatch, cfg=cfg, out=hout)
+    barrier()
+    e2e_times = []
+    for _ in range(max(3, args.steps // 2)):
+        t0 = time.perf_counter()
+        solver.solve_batch(hbatch, cfg=cfg, out=hout)
+        e2e_times.append(time.perf_counter() - t0)
+    e2e_s = statistics.median(e2e_times)
+    e2e_t = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(e2e_t, op=dist.ReduceOp.MAX)
+    e2e_value = world * N / float(e2e_t.item())
+    h2d = sum(a.nbytes for a in (hbatch.x0, hbatch.lower, hbatch.upper, hbatch.params))
+    d2h = (hout.x_star.nbytes + hout.f_star.nbytes + hout.pg_norm.nbytes + hout.status.nbytes +
+           hout.iterations.nbytes + hout.cg_iterations.nbytes + hout.f_evals.nbytes + hout.per_problem_time.nbytes +
+           hout.flops.nbytes)
+
+    # ---- CPU baseline (rank 0, N=1 only): the reference's solve_batch
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            from oracle import pyoracle
+
+            if pyoracle.ref_available():
+                cores = os.cpu_count() or 1
+                sample, n = cpu_sample(batch, seconds_target=2.0, workers=cores)
+                cpu_reference_run(sample, cores)
+                v, _ = cpu_reference_run(sample, cores, reps=3)
+                cpu = {"value": v, "unit": "solves/s", "cores": cores, "kind": "reference",
+                       "sample": f"first {n} of the {N} C2 problems, reference solve_batch(workers={cores}), best of 3"}
+        except Exception as e:
+            cpu = {"value": None, "unit": "solves/s", "cores": None, "kind": "reference", "sample": f"failed: {e}"}
+
+    traffic = None
+    prof = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(prof):
+        try:
+            traffic = json.load(open(prof)).get("bytes_per_launch")
+        except Exception:
+            traffic = None
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "solves/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": WORKLOAD, "family": "branch", "dim": DIM, "batch_per_gpu": N,
+                       "global_batch": world * N, "seed": "2+rank", "parallelism": f"batch sharded over {world} GPU(s)",
+                       "l2": "flushed (256 MiB write) between timed steps, outside the events", "mode": "exact"},
+            "e2e": {"value": e2e_value, "unit": "solves/s", "h2d_bytes_per_step": int(h2d),
+                    "d2h_bytes_per_step": int(d2h)},
+            "roofline": {"bound": "fp64", "achieved": achieved_tflops, "peak": fp64_peak, "unit": "TFLOP/s",
+                         "frac": achieved_tflops / fp64_peak if fp64_peak else None, "traffic": traffic,
+                         "peak_source": "DFMA microbenchmark measured in this run (tb_measure_fp64_peak)",
+                         "flops_per_launch": flops_per_launch,
+                         "flop_model": "algorithmic flops per SURVEY 8(d)/DESIGN.md, counted per problem on device"},
+            "cpu_baseline": cpu,
+            "clocks": clocks.summary(),
+            "gpu_launches": int(launches),
+            "parity": parity,
+            "status_counts": {str(k): int(v) for k, v in zip(*np.unique(status, return_counts=True))},
+            "ms_per_step_all": ms_steps,
+        }
+        print(json.dumps(line), flush=True)
+    solver.close()
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

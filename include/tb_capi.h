@@ -148,6 +148,10 @@ const char* tb_last_error(void);
 /* Number of solver-kernel launches issued since load (evidence counter). */
 int64_t tb_kernel_launch_count(void);
 
+/* FP64 DFMA throughput of `device` in TFLOP/s (the roofline denominator of
+ * the TRON kernel; measured, not nominal). */
+int tb_measure_fp64_peak(int32_t device, double* tflops);
+
 #ifdef __cplusplus
 }
 #endif

@@ -107,6 +107,7 @@ SIGNATURES = {
     ),
     "tb_last_error": (C.c_char_p, []),
     "tb_kernel_launch_count": (C.c_int64, []),
+    "tb_measure_fp64_peak": (C.c_int, [C.c_int32, C.POINTER(C.c_double)]),
 }
 
 _lib = None
