@@ -136,7 +136,7 @@ def run_reference_arm(args, rank, world):
         v, _ = cpu_reference_run(sample, cores)
         vals.append(v)
     wall = time.perf_counter() - t0
-    value = world * statistics.median(vals) if False else statistics.median(vals)
+    value = statistics.median(vals)
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "solves/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * wall / args.steps,
@@ -192,7 +192,10 @@ def main():
     dbatch = ProblemBatch(batch.family, batch.dim, t(batch.lower), t(batch.upper), t(batch.params), t(batch.x0))
     dout = Solver.alloc_result(N, DIM, device=True)
     flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)  # > 126 MB L2
-    stream = torch.cuda.current_stream(dev)
+    # a dedicated (non-default) stream: the kernel and the timing events are
+    # enqueued on the same stream handle
+    stream = torch.cuda.Stream(dev)
+    torch.cuda.set_stream(stream)
 
     def device_step():
         solver.solve_batch(dbatch, cfg=cfg, out=dout, stream=stream.cuda_stream)
@@ -256,9 +259,11 @@ def main():
     hbatch = ProblemBatch(batch.family, DIM, pinned(batch.lower), pinned(batch.upper), pinned(batch.params),
                           pinned(batch.x0))
     hout = Solver.alloc_result(N, DIM, device=False)
-    for name in ("x_star", "f_star", "pg_norm", "per_problem_time"):
+    tdt = {np.dtype(np.float64): torch.float64, np.dtype(np.int32): torch.int32, np.dtype(np.int64): torch.int64}
+    for name in ("x_star", "f_star", "pg_norm", "status", "iterations", "cg_iterations", "f_evals",
+                 "per_problem_time", "flops"):
         a = getattr(hout, name)
-        setattr(hout, name, pinned(np.zeros(a.shape)))
+        setattr(hout, name, torch.empty(a.shape, dtype=tdt[a.dtype], pin_memory=True).numpy())
     for _ in range(2):
         solver.solve_batch(hbatch, cfg=cfg, out=hout)
     barrier()

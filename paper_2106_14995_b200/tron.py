@@ -240,7 +240,10 @@ class Solver:
         r.memspace = L.TB_MEM_DEVICE if _is_device(out.status) else L.TB_MEM_HOST
         c = cfg.to_c()
         if stream is not None:
-            rc = self._lib.tb_solve_batch_async(self._ctx, C.byref(b), C.byref(c), C.byref(r), C.c_void_p(stream))
+            # 0 is the legacy default stream (torch's default): pass it as
+            # cudaStreamLegacy (0x1); NULL would select the context stream
+            h = int(stream) if int(stream) != 0 else 1
+            rc = self._lib.tb_solve_batch_async(self._ctx, C.byref(b), C.byref(c), C.byref(r), C.c_void_p(h))
             if rc != L.TB_OK:
                 _raise(rc)
             return out
