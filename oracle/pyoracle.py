@@ -91,6 +91,8 @@ class Result:
         self.cg_iterations = np.zeros(N, np.int64)
         self.f_evals = np.zeros(N, np.int64)
         self.flops = np.zeros(N, np.int64)
+        self.executed = np.zeros(N, np.int32)
+        self.ff_iter = np.zeros(N, np.int32)
         self.per_problem_time = np.zeros(N)
         self.batch_wall_time = 0.0
         self.rc = 0
@@ -103,6 +105,11 @@ def _arrays(batch, x0):
     prm = None if batch.params is None else np.ascontiguousarray(batch.params, dtype=np.float64)
     stride = 0 if prm is None else prm.shape[1]
     return x0, lo, up, prm, stride
+
+
+def set_fast_forward(on: bool) -> None:
+    """Opt-in replay-skip of zero-change fixed points in the C restatement."""
+    oracle_lib().fn("set_fast_forward")(1 if on else 0)
 
 
 def solve_batch(batch, x0=None, cfg=None, workers=1, impl="oracle") -> Result:
@@ -120,7 +127,7 @@ def solve_batch(batch, x0=None, cfg=None, workers=1, impl="oracle") -> Result:
         r.rc = f(int(batch.family), n, C.c_int64(N), _p(x0), _p(lo), _p(up), _p(prm), C.c_int64(stride),
                  C.byref(c), int(workers), _p(r.x_star), _p(r.f_star), _p(r.pg_norm), _p(r.status, ip),
                  _p(r.iterations, ip), _p(r.cg_iterations, lp), _p(r.f_evals, lp), _p(r.flops, lp),
-                 C.byref(wall))
+                 _p(r.executed, ip), _p(r.ff_iter, ip), C.byref(wall))
     else:
         f = ref_lib().fn("solve_batch")
         f.restype = C.c_int

@@ -18,6 +18,9 @@
 #include "../paper_2106_14995_b200/csrc/tb_flops.h"
 
 static __thread long long g_fl; /* per-thread flop counter of the current solve */
+static int g_fast_forward = 0; /* opt-in: replay-skip of zero-change fixed points */
+
+void orc_set_fast_forward(int on) { g_fast_forward = on; }
 
 #define SMAX tb_smax /* std::max semantics */
 #define SMIN tb_smin /* std::min semantics */
@@ -539,10 +542,13 @@ int orc_solve(const orc_problem* p, const double* x0, const tb_tron_config* cfg,
     if (rep->status != TB_STATUS_CONVERGED) {
         for (int iter = 1; iter <= cfg->max_iter; ++iter) {
             rep->iterations = iter;
+            ++rep->executed_iterations;
             if (need_hessian) {
                 p->hess(p->ctx, x, A);
                 need_hessian = 0;
             }
+            const long long fl_iter0 = g_fl;
+            const double delta_in = delta, alpha_in = alpha_c;
             double cs[m];
             double alpha_new;
             if ((rc = orc_cauchy(n, x, g, A, l, u, delta, cfg, alpha_c, &alpha_new, cs))) {
@@ -589,7 +595,8 @@ int orc_solve(const orc_problem* p, const double* x0, const tb_tron_config* cfg,
             delta = SMIN(delta, cfg->delta_max);
             g_fl += 12;
 
-            if (actred > cfg->eta0 * prered) {
+            const int accepted = actred > cfg->eta0 * prered;
+            if (accepted) {
                 memcpy(x, xs, sizeof(double) * n);
                 f = f_trial;
                 p->grad(p->ctx, x, g);
@@ -601,6 +608,20 @@ int orc_solve(const orc_problem* p, const double* x0, const tb_tron_config* cfg,
                 }
             }
             if (delta <= 1e-300) break;
+            /* a rejected iteration k >= 2 leaving delta and
+             * alpha_c unchanged leaves the whole state unchanged; the rest of
+             * the loop replays it (same counters each time). */
+            if (!accepted && iter >= 2 && delta == delta_in && alpha_c == alpha_in) {
+                if (!rep->ff_iter) rep->ff_iter = iter;
+                if (g_fast_forward) {
+                    const long long rem = cfg->max_iter - iter;
+                    rep->cg_iterations += rem * cg_its;
+                    rep->f_evals += rem;
+                    g_fl += rem * (g_fl - fl_iter0);
+                    rep->iterations = cfg->max_iter;
+                    break;
+                }
+            }
         }
     }
     free(A);
@@ -660,6 +681,7 @@ typedef struct {
     double *x_star, *f_star, *pg_norm;
     int32_t *status, *iterations;
     int64_t *cg_iterations, *f_evals, *flops;
+    int32_t *executed, *ff_iter;
     int err;
 } chunk_t;
 
@@ -679,6 +701,8 @@ static void* run_chunk(void* arg) {
         if (c->cg_iterations) c->cg_iterations[i] = rep.cg_iterations;
         if (c->f_evals) c->f_evals[i] = rep.f_evals;
         if (c->flops) c->flops[i] = rep.flops;
+        if (c->executed) c->executed[i] = rep.executed_iterations;
+        if (c->ff_iter) c->ff_iter[i] = rep.ff_iter;
         if (rc && !c->err) c->err = rc; /* reference aborts the chunk; we record */
     }
     return NULL;
@@ -694,7 +718,8 @@ int orc_solve_batch(int family, int n, int64_t count, const double* x0, const do
                     const double* upper, const double* params, int64_t params_stride,
                     const tb_tron_config* cfg, int workers, double* x_star, double* f_star,
                     double* pg_norm, int32_t* status, int32_t* iterations, int64_t* cg_iterations,
-                    int64_t* f_evals, int64_t* flops, double* batch_wall_time) {
+                    int64_t* f_evals, int64_t* flops, int32_t* executed, int32_t* ff_iter,
+                    double* batch_wall_time) {
     if (workers < 1) return TB_E_INVALID_ARGUMENT;
     chunk_t* ch = (chunk_t*)calloc((size_t)workers, sizeof(chunk_t));
     pthread_t* th = (pthread_t*)calloc((size_t)workers, sizeof(pthread_t));
@@ -704,7 +729,8 @@ int orc_solve_batch(int family, int n, int64_t count, const double* x0, const do
     for (int k = 0; k < workers; ++k) {
         const int64_t hi = lo + base + (k < rem ? 1 : 0);
         chunk_t c = {family, n, lo, hi, x0, lower, upper, params, params_stride, cfg,
-                     x_star, f_star, pg_norm, status, iterations, cg_iterations, f_evals, flops, 0};
+                     x_star, f_star, pg_norm, status, iterations, cg_iterations, f_evals, flops,
+                     executed, ff_iter, 0};
         ch[k] = c;
         lo = hi;
     }

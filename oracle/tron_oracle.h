@@ -40,7 +40,12 @@ typedef struct orc_report {
     int64_t cg_iterations;
     int64_t f_evals;
     int64_t flops; /* algorithmic flop model */
+    int32_t executed_iterations; /* loop iterations actually run */
+    int32_t ff_iter;             /* first zero-change fixed-point iteration, 0 if none */
 } orc_report;
+
+/* Opt-in fast-forward of zero-change fixed points (as the device does). */
+void orc_set_fast_forward(int on);
 
 /* dense.hpp */
 void orc_axpy(int n, double alpha, const double* x, double* y);
@@ -96,7 +101,8 @@ int orc_solve_batch(int family, int n, int64_t count, const double* x0, const do
                     const double* upper, const double* params, int64_t params_stride,
                     const tb_tron_config* cfg, int workers, double* x_star, double* f_star,
                     double* pg_norm, int32_t* status, int32_t* iterations, int64_t* cg_iterations,
-                    int64_t* f_evals, int64_t* flops, double* batch_wall_time);
+                    int64_t* f_evals, int64_t* flops, int32_t* executed, int32_t* ff_iter,
+                    double* batch_wall_time);
 /* family f/grad/Hessian (for derivative tests) */
 void orc_family_eval(int family, int n, const double* x, const double* params, double* f,
                      double* g, double* H);

@@ -48,3 +48,163 @@ def test_hs45(solver, d):
     xs = host(res.x_star)
     assert (host(res.status) == 0).all()
     assert np.abs(xs - np.arange(1, d + 1)).max() <= 1e-6
+
+
+# ---------------------------------------------------------------- fixtures
+import glob  # noqa: E402
+import os  # noqa: E402
+from types import SimpleNamespace  # noqa: E402
+
+from conftest import FIELDS  # noqa: E402
+from paper_2106_14995_b200 import (  # noqa: E402
+    EvaluationError, ProblemBatch, Solver, SolveStatus, TronConfig)
+
+GOLDEN = sorted(glob.glob(os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "*.npz")))
+
+
+@pytest.mark.parametrize("path", GOLDEN, ids=[os.path.basename(p)[:-4] for p in GOLDEN])
+def test_device_matches_reference_golden(solver, path):
+    """Fixtures hold the REFERENCE's own outputs (tests/golden/make_golden.py)."""
+    g = np.load(path)
+    prm = g["params"] if g["params"].shape[1] else None
+    b = ProblemBatch(int(g["family"]), int(g["dim"]), g["lower"], g["upper"], prm, g["x0"])
+    res = solver.solve_batch(b)
+    assert_bitwise(res, SimpleNamespace(**{k: g[k] for k in FIELDS}), label=os.path.basename(path))
+
+
+def test_c2_full_size_bitwise(solver):
+    """BASELINE configs[1] at full size: 65,536 branch6 problems, every field
+    bit-identical to the CPU oracle (restatement pinned to the reference)."""
+    b = synth.branch(65536, 6, seed=2)
+    res = solver.solve_batch(b)
+    ref = po.solve_batch(b, impl="oracle", workers=os.cpu_count() or 8)
+    assert_bitwise(res, ref, label="C2 65536")
+    st = host(res.status)
+    assert (st <= 1).all() and (st == 1).mean() < 0.02
+
+
+def test_boxqp_matches_bruteforce_active_set_oracle(solver):
+    """SPEC acceptance 5 / tron_test.cpp:196-212 at 50 problems."""
+    import ctypes as C
+
+    b = synth.boxqp(50, 4, seed=21)
+    res = solver.solve_batch(b)
+    assert (host(res.status) == 0).all()
+    xs = host(res.x_star)
+    for k in range(50):
+        H = np.ascontiguousarray(b.params[k, :16])
+        c = np.ascontiguousarray(b.params[k, 16:])
+        lo, up = np.ascontiguousarray(b.lower[k]), np.ascontiguousarray(b.upper[k])
+        x = np.zeros(4)
+        if po.ref_available():
+            f = po.ref_lib().fn("boxqp_oracle")
+            assert f(4, H.ctypes.data_as(po.dp), c.ctypes.data_as(po.dp), lo.ctypes.data_as(po.dp),
+                     up.ctypes.data_as(po.dp), x.ctypes.data_as(po.dp)) == 0
+            assert np.max(np.abs(xs[k] - x)) <= 1e-6
+
+
+def test_empty_batch(solver):
+    b = synth.ncvx(0, 4)
+    res = solver.solve_batch(b)
+    assert host(res.status).shape == (0,)
+
+
+def test_start_outside_box_and_infinite_bounds(solver):
+    """tron.hpp:473 (x0 is projected, never rejected); tron.hpp:17 (+-inf)."""
+    b = synth.boxqp(256, 5, seed=8)
+    b.lower[::3, 1] = -np.inf
+    b.upper[::4, 2] = np.inf
+    x0 = b.x0 * 5.0
+    res = solver.solve_batch(b, x0)
+    ref = po.solve_batch(b, x0, impl="oracle")
+    assert_bitwise(res, ref, label="outside/inf")
+    xs = host(res.x_star)
+    assert (xs >= b.lower).all() and (xs <= b.upper).all()
+
+
+@pytest.mark.parametrize("cfg", [TronConfig(max_iter=1), TronConfig(delta0=0.3), TronConfig(tol_pg=1e-9),
+                                 TronConfig(cg_tol=0.5, mu0=0.1, interp_factor=0.25),
+                                 TronConfig(sigma1=0.1, sigma2=0.3, sigma3=2.0, eta0=0.01, delta_max=5.0)])
+def test_config_variants_bitwise(solver, cfg):
+    for b in (synth.ncvx(256, 6, seed=4), synth.branch(256, 6, seed=4), synth.hs45(2, 8)):
+        assert_bitwise(solver.solve_batch(b, cfg=cfg), po.solve_batch(b, cfg=cfg, impl="oracle"), label=str(cfg))
+
+
+def test_iteration_limit_status(solver):
+    """tron_test.cpp:242-249 intent (IterLimit at max_iter=1) on a problem that
+    does not converge in one iteration."""
+    b = synth.ncvx(64, 8, seed=2)
+    res = solver.solve_batch(b, cfg=TronConfig(max_iter=1))
+    st, it = host(res.status), host(res.iterations)
+    assert ((st == 1) & (it == 1)).sum() > 0
+    assert_bitwise(res, po.solve_batch(b, cfg=TronConfig(max_iter=1), impl="oracle"))
+
+
+def test_nan_hessian_factorization_failed(solver):
+    """tron_test.cpp:251-266: a NaN Hessian diagonal -> FactorizationFailed
+    (NaN pivots fail until the shift cap, dense.hpp:197-199)."""
+    b = synth.boxqp(8, 2, seed=3)
+    b.params[:, 3] = np.nan  # H(1,1)
+    res = solver.solve_batch(b)
+    ref = po.solve_batch(b, impl="oracle")
+    assert_bitwise(res, ref, label="nan hessian")
+    assert (host(res.status) == SolveStatus.FactorizationFailed).any()
+
+
+def test_evaluation_error_raises_like_reference(solver):
+    """tron.hpp:190-194: a non-finite Cauchy model throws EvaluationError out
+    of solve_batch (batch.hpp:75-76); the device raises the same type."""
+    b = synth.boxqp(4, 3, seed=6)
+    b.params[2, 0] = np.inf  # H(0,0) = inf in problem 2
+    with pytest.raises(EvaluationError):
+        solver.solve_batch(b)
+    ref = po.solve_batch(b, impl="oracle")
+    assert ref.rc == SolveStatus.EvaluationError
+
+
+def test_invalid_bounds_raise(solver):
+    b = synth.ncvx(4, 3)
+    b.lower[1, 0] = b.upper[1, 0] + 1.0
+    with pytest.raises(ValueError, match="lower bound exceeds upper bound"):
+        solver.solve_batch(b)
+
+
+def test_fast_forward_on_device_is_neutral():
+    b = synth.branch(8192, 6, seed=5)
+    a = Solver((0,), fast_forward=True).solve_batch(b)
+    z = Solver((0,), fast_forward=False).solve_batch(b)
+    assert_bitwise(a, z, label="device ff")
+    assert np.array_equal(host(a.flops), host(z.flops))
+
+
+def test_device_memspace_and_stream_async(solver):
+    import torch
+
+    b = synth.branch(4096, 6, seed=12)
+    dev = torch.device("cuda", 0)
+    t = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(dev)  # noqa: E731
+    db = ProblemBatch(b.family, 6, t(b.lower), t(b.upper), t(b.params), t(b.x0))
+    r1 = solver.solve_batch(db)  # blocking, device memspace
+    s = torch.cuda.Stream(dev)
+    out = Solver.alloc_result(b.count, 6, device=True)
+    solver.solve_batch(db, out=out, stream=s.cuda_stream)
+    s.synchronize()
+    ref = po.solve_batch(b, impl="oracle", workers=8)
+    assert_bitwise(r1, ref, label="device memspace")
+    assert_bitwise(out, ref, label="async stream")
+
+
+def test_dimension_over_warp_capacity_rejected(solver):
+    with pytest.raises(ValueError):
+        solver.solve_batch(synth.ncvx(2, 33))
+
+
+def test_hs45_acceptance_all_n(solver):
+    """SPEC acceptance 1: n = 1..32 converge with x*_i = i and f* = 120 - n!."""
+    import math
+
+    for n in range(1, 33):
+        res = solver.solve_batch(synth.hs45(1, n))
+        assert host(res.status)[0] == 0
+        assert np.abs(host(res.x_star)[0] - np.arange(1, n + 1)).max() <= 1e-6
+        assert abs(host(res.f_star)[0] - (120.0 - math.factorial(n))) <= 1e-9 * max(1.0, math.factorial(n))
