@@ -141,14 +141,19 @@ def test_iteration_limit_status(solver):
 
 
 def test_nan_hessian_factorization_failed(solver):
-    """tron_test.cpp:251-266: a NaN Hessian diagonal -> FactorizationFailed
-    (NaN pivots fail until the shift cap, dense.hpp:197-199)."""
-    b = synth.boxqp(8, 2, seed=3)
-    b.params[:, 3] = np.nan  # H(1,1)
+    """tron_test.cpp:251-266: H = [[1, 0], [0, NaN]] with a zero second
+    gradient component (the gemv zero-skip, dense.hpp:110, keeps the Cauchy
+    model finite); the NaN pivot fails every shift until the cap
+    (dense.hpp:197-199) -> FactorizationFailed."""
+    H = np.array([1.0, 0.0, 0.0, np.nan])  # column-major
+    c = np.array([0.0, 0.5])
+    prm = np.tile(np.concatenate([H, c]), (3, 1))
+    b = ProblemBatch(1, 2, np.full((3, 2), -1.0), np.full((3, 2), 1.0), prm, np.tile([0.5, 0.5], (3, 1)))
     res = solver.solve_batch(b)
     ref = po.solve_batch(b, impl="oracle")
     assert_bitwise(res, ref, label="nan hessian")
-    assert (host(res.status) == SolveStatus.FactorizationFailed).any()
+    assert (host(res.status) == SolveStatus.FactorizationFailed).all()
+    assert (host(res.iterations) == 1).all()
 
 
 def test_evaluation_error_raises_like_reference(solver):
@@ -208,3 +213,17 @@ def test_hs45_acceptance_all_n(solver):
         assert host(res.status)[0] == 0
         assert np.abs(host(res.x_star)[0] - np.arange(1, n + 1)).max() <= 1e-6
         assert abs(host(res.f_star)[0] - (120.0 - math.factorial(n))) <= 1e-9 * max(1.0, math.factorial(n))
+
+
+def test_cpp_dropin_against_reference_solve_batch():
+    """include/tronbatch_gpu/solve_batch.hpp used exactly like the reference
+    API (tests/cpp/gpu_dropin_test.cpp), compared with the reference's own
+    CPU solve_batch in the same process (built with the reference headers)."""
+    import subprocess
+
+    exe = os.path.join(os.path.dirname(po.HERE), "oracle", "_ref", "gpu_dropin_test")
+    if not os.path.exists(exe):
+        pytest.skip("gpu_dropin_test not built (needs /root/reference at build time)")
+    p = subprocess.run([exe], capture_output=True, text=True, timeout=300)
+    assert p.returncode == 0, p.stdout + p.stderr
+    assert '"failed": 0' in p.stdout
