@@ -242,7 +242,10 @@ def main():
     ms_per_step = ms_total / args.steps
     value = world * N / (ms_per_step * 1e-3)
 
-    # ---- algorithmic flops per launch (device counters; deterministic)
+    # ---- algorithmic flops per launch: one untimed run of the counting
+    # variant (identical results; the count is deterministic)
+    solver.solve_batch(dbatch, cfg=cfg, out=dout, stream=stream.cuda_stream, count_flops=True)
+    torch.cuda.synchronize(dev)
     flops_per_launch = float(dout.flops.sum().item())
     status = dout.status.cpu().numpy()
     achieved_tflops = flops_per_launch / (ms_per_step * 1e-3) / 1e12

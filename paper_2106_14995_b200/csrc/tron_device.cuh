@@ -7,16 +7,23 @@
 // scalar of the algorithm (f, delta, alpha, rho, ...) is computed redundantly
 // and identically by all 32 lanes, so control flow is warp-uniform.
 //
+// D is a compile-time bound (the exact dimension for the branch family, the
+// next power of two otherwise); small-D kernels are fully unrolled.
+//
 // The free-set sub-systems of subspace_step (tron.hpp:405-411: B = A[F,F],
 // compacted) are NOT compacted: every routine takes a lane mask F and walks
-// the free indices in ascending order (set-bit iteration), which reproduces
-// the compacted loops operation for operation.
+// the free indices in ascending order, which reproduces the compacted loops
+// operation for operation.
 //
 // Exact mode (nvcc --fmad=false): every reduction whose order matters is
 // summed sequentially in ascending index order exactly like dense.hpp:79-84
-// (dot) and dense.hpp:230-234 (backward solve); min/max and counting
-// reductions (order-independent for the values they see) use warp shuffles.
-// Results are bit-identical to the reference compiled with -ffp-contract=off.
+// (dot) and dense.hpp:230-234 (backward solve).  Ordered sums run over all D
+// slots with +0.0 in the masked-out ones: a sum that starts at +0.0 and only
+// adds can never be -0.0 (round-to-nearest), so s + 0.0 == s bit-for-bit and
+// the padded sum equals the reference's sum over the free indices.  min/max
+// and counting reductions (order-independent for the non-negative values they
+// see) use integer warp reductions on the IEEE bit patterns.  Results are
+// bit-identical to the reference compiled with -ffp-contract=off.
 #pragma once
 
 #include <cuda_runtime.h>
@@ -35,6 +42,21 @@ __device__ __forceinline__ int lane_id() { return threadIdx.x & 31; }
 __device__ __forceinline__ bool in_mask(unsigned m, int i) { return (m >> i) & 1u; }
 __device__ __forceinline__ int low_bit(unsigned m) { return __ffs(m) - 1; }
 __device__ __forceinline__ int high_bit(unsigned m) { return 31 - __clz(m); }
+
+// max / min over the warp of NON-NEGATIVE doubles (+0.0 .. +inf, no NaN):
+// IEEE bit patterns of such values order like unsigned integers.
+__device__ __forceinline__ double warp_max_nonneg(double v) {
+    const unsigned long long b = __double_as_longlong(v);
+    const unsigned hi = __reduce_max_sync(FULL, (unsigned)(b >> 32));
+    const unsigned lo = __reduce_max_sync(FULL, (unsigned)(b >> 32) == hi ? (unsigned)b : 0u);
+    return __longlong_as_double((long long)(((unsigned long long)hi << 32) | lo));
+}
+__device__ __forceinline__ double warp_min_nonneg(double v) {
+    const unsigned long long b = __double_as_longlong(v);
+    const unsigned hi = __reduce_min_sync(FULL, (unsigned)(b >> 32));
+    const unsigned lo = __reduce_min_sync(FULL, (unsigned)(b >> 32) == hi ? (unsigned)b : 0xffffffffu);
+    return __longlong_as_double((long long)(((unsigned long long)hi << 32) | lo));
+}
 
 struct KernelArgs {
     int n;
@@ -58,70 +80,74 @@ struct KernelArgs {
     int64_t* flops;
 };
 
-// shared memory per warp (doubles)
+// shared memory per warp (doubles; every region starts at an even offset)
 template <int D>
 struct SmemLayout {
-    static constexpr int A = 0;                 // D*D Hessian
-    static constexpr int L = A + D * D;         // D*D factor
-    static constexpr int BUF = L + D * D;       // 2*D ordered-sum staging (double buffered)
-    static constexpr int BB = BUF + 2 * D;      // D backward-solve results / second staging
-    static constexpr int XS = BB + D;           // D point for family evaluations
-    static constexpr int CTX = XS + D;          // family context (branch: sizeof(tb_branch_ctx))
-    static constexpr int CTX_DOUBLES = (int)(sizeof(tb_branch_ctx) / sizeof(double));
+    static constexpr int A = 0;              // D*D Hessian
+    static constexpr int L = A + D * D;      // D*D factor
+    static constexpr int S1 = L + D * D;     // 2*D ordered-sum staging (double buffered)
+    static constexpr int S2 = S1 + 2 * D;    // 2*D second staging (double buffered)
+    static constexpr int XS = S2 + 2 * D;    // D point for family evaluations
+    static constexpr int CTX = XS + D;       // family context (branch: sizeof(tb_branch_ctx))
+    static constexpr int CTX_DOUBLES = (int)((sizeof(tb_branch_ctx) / sizeof(double) + 1) & ~1);
     static constexpr int PRM = CTX + CTX_DOUBLES;  // staged parameters
     static constexpr int fixed() { return PRM; }
+    static_assert(D % 2 == 0, "D must be even (16-byte staging loads)");
 };
 
 // ---------------------------------------------------------------- per warp
-template <int D>
+template <int D, bool COUNT>
 struct Warp {
+    static constexpr bool kUnroll = D <= 8;
     double* A;
     double* L;
-    double* buf;  // 2*D
-    double* bb;   // D
-    double* xs;   // D
+    double* s1;  // 2*D
+    double* s2;  // 2*D
+    double* xs;  // D
     const double* prm;
     const tb_tron_config* cfg;
     int n;
     int lane;
-    int tog;        // ordered-sum buffer toggle (0 or D)
+    int tog;        // staging toggle (0 or D)
     unsigned act;   // lanes 0..n-1
-    long long fl;   // algorithmic flop counter (tb_flops.h model)
+    long long fl;   // algorithmic flop counter (tb_flops.h model), COUNT builds only
+
+    __device__ __forceinline__ void count(long long v) {
+        if (COUNT) fl += v;
+    }
 
     // ------------------------------------------------ ordered reductions
-    // sum_{j in m, ascending} v_j, starting from 0.0 (dense.hpp:81-83).
-    // Double-buffered staging: one __syncwarp per sum (the other buffer's
-    // readers are ordered by the previous sum's barrier).
-    __device__ __forceinline__ double seq_sum(double v, unsigned m) {
-        double* b = buf + tog;
-        tog ^= D;
-        if (lane < D) b[lane] = v;
-        __syncwarp();
+    // sum_{j in m, ascending} v_j from +0.0 (dense.hpp:81-83), zero-padded
+    __device__ __forceinline__ double padded_sum(const double* b) {
         double s = 0.0;
 #pragma unroll
-        for (int j = 0; j < D; ++j)
-            if (in_mask(m, j)) s += b[j];
+        for (int j = 0; j < D; j += 2) {
+            const double2 t = *reinterpret_cast<const double2*>(b + j);
+            s += t.x;
+            s += t.y;
+        }
         return s;
     }
-    // two/three independent ordered sums (same bits as separate calls)
-    __device__ __forceinline__ void seq_sum2(double a, double c, unsigned m, double& sa, double& sc) {
-        double* b = buf + tog;
+    __device__ __forceinline__ double seq_sum(double v, unsigned m) {
+        double* b = s1 + tog;
         tog ^= D;
-        double* b2 = bb;
+        if (lane < D) b[lane] = in_mask(m, lane) ? v : 0.0;
+        __syncwarp();
+        return padded_sum(b);
+    }
+    // two independent ordered sums, one barrier
+    __device__ __forceinline__ void seq_sum2(double a, double c, unsigned m, double& sa, double& sc) {
+        double* b = s1 + tog;
+        double* b2 = s2 + tog;
+        tog ^= D;
         if (lane < D) {
-            b[lane] = a;
-            b2[lane] = c;
+            const bool in = in_mask(m, lane);
+            b[lane] = in ? a : 0.0;
+            b2[lane] = in ? c : 0.0;
         }
         __syncwarp();
-        sa = 0.0;
-        sc = 0.0;
-#pragma unroll
-        for (int j = 0; j < D; ++j)
-            if (in_mask(m, j)) {
-                sa += b[j];
-                sc += b2[j];
-            }
-        __syncwarp();  // bb is not double buffered
+        sa = padded_sum(b);
+        sc = padded_sum(b2);
     }
     __device__ __forceinline__ void seq_sum3(double a, double c, double e, unsigned m, double& sa, double& sc,
                                              double& se) {
@@ -129,44 +155,40 @@ struct Warp {
         se = seq_sum(e, m);
     }
     __device__ __forceinline__ double dot(double x, double y, unsigned m) {
-        fl += 2 * __popc(m);
+        count(2 * __popc(m));
         return seq_sum(x * y, m);
     }
     __device__ __forceinline__ double nrm2(double x, unsigned m) {
-        fl += 1;
+        count(1);
         return sqrt(dot(x, x, m));
-    }
-    __device__ __forceinline__ double wmax(double v) {
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(FULL, v, o));
-        return v;
-    }
-    __device__ __forceinline__ double wmin(double v) {
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) v = fmin(v, __shfl_xor_sync(FULL, v, o));
-        return v;
     }
     __device__ __forceinline__ double bcast(double v, int src) { return __shfl_sync(FULL, v, src); }
 
     // y = A[m,m] x over the lanes in m; dense.hpp:104-112 (alpha=1, beta=0):
-    // column sweep j ascending, zero-skip on x_j.
+    // column sweep j ascending, zero-skip on x_j (masked columns staged as 0)
     __device__ __forceinline__ double gemv(double x, unsigned m) {
-        double* b = buf + tog;
+        double* b = s1 + tog;
         tog ^= D;
-        if (lane < D) b[lane] = x;
+        if (lane < D) b[lane] = in_mask(m, lane) ? x : 0.0;
         __syncwarp();
-        const int nm = __popc(m);
         double y = 0.0 * 0.0;
         int used = 0;
+        if (lane < D) {
 #pragma unroll
-        for (int j = 0; j < D; ++j) {
-            if (!in_mask(m, j)) continue;
-            const double xj = 1.0 * b[j];
-            if (xj == 0.0) continue;
-            y += xj * A[lane + j * D];
-            ++used;
+            for (int j = 0; j < D; j += 2) {
+                const double2 t = *reinterpret_cast<const double2*>(b + j);
+                const double x0 = 1.0 * t.x, x1 = 1.0 * t.y;
+                if (x0 != 0.0) {
+                    y += x0 * A[lane + j * D];
+                    ++used;
+                }
+                if (x1 != 0.0) {
+                    y += x1 * A[lane + (j + 1) * D];
+                    ++used;
+                }
+            }
         }
-        fl += 2 * nm * used;
+        if (COUNT) fl += 2LL * __popc(m) * __shfl_sync(FULL, used, 0);
         return y;
     }
 
@@ -174,16 +196,17 @@ struct Warp {
     __device__ __forceinline__ double clip(double x, double l, double u) { return tb_smin(tb_smax(x, l), u); }
     // tron.hpp:129-138
     __device__ __forceinline__ double gpstep(double x, double alpha, double w, double l, double u, unsigned m) {
-        fl += 2 * __popc(m);
+        count(2 * __popc(m));
         const double trial = x + alpha * w;
         if (trial < l) return l - x;
         if (trial > u) return u - x;
         return alpha * w;
     }
-    // tron.hpp:147-164 (min/max over finite breakpoints are order-free)
+    // tron.hpp:147-164: breakpoints are finite and > 0 (x strictly inside the
+    // bound it moves to), so min/max are order-free integer reductions
     __device__ __forceinline__ void breakpt(double x, double w, double l, double u, unsigned m, double& bmin,
                                             double& bmax) {
-        fl += 2 * __popc(m);
+        count(2 * __popc(m));
         double b = 0.0;
         bool has = false;
         if (in_mask(m, lane)) {
@@ -196,8 +219,8 @@ struct Warp {
             bmax = 0.0;
             return;
         }
-        bmin = wmin(has ? b : CUDART_INF);
-        bmax = wmax(has ? b : -CUDART_INF);
+        bmin = warp_min_nonneg(has ? b : CUDART_INF);
+        bmax = warp_max_nonneg(has ? b : 0.0);
     }
     // tron.hpp:112-121: inf-norm of the projected gradient; NaN components are
     // ignored by std::max, so they contribute 0
@@ -207,13 +230,13 @@ struct Warp {
         else if (x >= u) pg = tb_smax(g, 0.0);
         double v = fabs(pg);
         if (!(lane < n) || isnan(v)) v = 0.0;
-        return wmax(v);
+        return warp_max_nonneg(v);
     }
     // tron.hpp:167-176.  Returns 0 or TB_STATUS_ZERO_DIRECTION.
     __device__ __forceinline__ int trqsol(double x, double w, double delta, unsigned m, double& sigma) {
         double ptx, ptp, xtx;
         seq_sum3(w * x, w * w, x * x, m, ptx, ptp, xtx);
-        fl += 6 * __popc(m) + 8;
+        count(6 * __popc(m) + 8);
         if (ptp == 0.0) return TB_STATUS_ZERO_DIRECTION;
         const double dsq = delta * delta;
         const double rad = sqrt(tb_smax(ptx * ptx + ptp * tb_smax(dsq - xtx, 0.0), 0.0));
@@ -226,24 +249,28 @@ struct Warp {
         const double as = gemv(s, m);
         double sas;
         seq_sum2(g * s, s * as, m, gs, sas);
-        fl += 4 * __popc(m) + 2;
+        count(4 * __popc(m) + 2);
         return gs + 0.5 * sas;
     }
 
     // ------------------------------------------------ dense.hpp factorization
-    // dense.hpp:138-156 on A[F,F]: left-looking, zero-skip on L(j,k), pivot
-    // test !(pivot > 0), divide by sqrt(pivot).  Lane i keeps L(i,j) of the
-    // current column in a register.
-    __device__ __forceinline__ bool chol_left(unsigned F, int nf, double shift) {
-        const bool inF = in_mask(F, lane);
-        int rem = nf;  // free rows at or below the current column
-#pragma unroll 1
-        for (unsigned mj = F; mj; mj &= mj - 1) {
-            const int j = low_bit(mj);
-            const bool row = inF && lane >= j;
-            double lij = row ? A[lane + j * D] : 0.0;
-            if (lane == j) lij += shift;
-            long long cnt = 0;
+    // one column of dense.hpp:141-154 (left-looking, zero-skip on L(j,k),
+    // pivot test !(pivot > 0), division by sqrt(pivot))
+    __device__ __forceinline__ bool chol_column(unsigned F, int j, double shift, int rem) {
+        const bool row = in_mask(F, lane) && lane >= j;
+        double lij = row ? A[lane + j * D] : 0.0;
+        if (lane == j) lij += shift;
+        long long cnt = 0;
+        if (kUnroll) {
+#pragma unroll
+            for (int k = 0; k < D - 1; ++k) {
+                if (k >= j || !in_mask(F, k)) continue;
+                const double ljk = L[j + k * D];
+                if (ljk == 0.0) continue;
+                if (row) lij -= ljk * L[lane + k * D];
+                ++cnt;
+            }
+        } else {
 #pragma unroll 1
             for (unsigned mk = F & ((1u << j) - 1u); mk; mk &= mk - 1) {
                 const int k = low_bit(mk);
@@ -252,16 +279,33 @@ struct Warp {
                 if (row) lij -= ljk * L[lane + k * D];
                 ++cnt;
             }
-            fl += 1 + 2 * rem * cnt;
-            const double pivot = bcast(lij, j);
-            if (!(pivot > 0.0)) return false;
-            const double d = sqrt(pivot);
-            if (lane == j) lij = d;
-            else if (row) lij = lij / d;
-            if (row) L[lane + j * D] = lij;
-            fl += rem;  // sqrt + (rem - 1) divisions
-            --rem;
-            __syncwarp();
+        }
+        count(1 + 2LL * rem * cnt);
+        const double pivot = bcast(lij, j);
+        if (!(pivot > 0.0)) return false;
+        const double d = sqrt(pivot);
+        const double q = lij / d;  // every lane (non-rows hold 0): no divergence
+        lij = lane == j ? d : q;
+        if (row) L[lane + j * D] = lij;
+        count(rem);  // sqrt + (rem - 1) divisions
+        __syncwarp();
+        return true;
+    }
+    __device__ __forceinline__ bool chol_left(unsigned F, int nf, double shift) {
+        int rem = nf;  // free rows at or below the current column
+        if (kUnroll) {
+#pragma unroll
+            for (int j = 0; j < D; ++j) {
+                if (!in_mask(F, j)) continue;
+                if (!chol_column(F, j, shift, rem)) return false;
+                --rem;
+            }
+        } else {
+#pragma unroll 1
+            for (unsigned mj = F; mj; mj &= mj - 1) {
+                if (!chol_column(F, low_bit(mj), shift, rem)) return false;
+                --rem;
+            }
         }
         return true;
     }
@@ -272,13 +316,15 @@ struct Warp {
         double dg = inF ? fabs(A[lane + lane * D]) : 0.0;
         if (isnan(dg)) dg = 0.0;
         double ma = 0.0;
+        if (inF) {
 #pragma unroll 1
-        for (unsigned mj = F; mj; mj &= mj - 1) {
-            const double v = fabs(A[lane + low_bit(mj) * D]);
-            if (inF && !isnan(v)) ma = fmax(ma, v);
+            for (unsigned mj = F; mj; mj &= mj - 1) {
+                const double v = fabs(A[lane + low_bit(mj) * D]);
+                if (!isnan(v)) ma = fmax(ma, v);
+            }
         }
-        const double max_diag = wmax(dg);
-        const double max_abs = wmax(ma);
+        const double max_diag = warp_max_nonneg(dg);
+        const double max_abs = warp_max_nonneg(ma);
         const double alpha0 = tb_smax(1e-3 * max_diag, 1e-8);
         const double cap = 1e8 * tb_smax(1.0, max_abs);
         double alpha = 0.0;
@@ -289,43 +335,69 @@ struct Warp {
                 return 0;
             }
             alpha = tb_smax(2.0 * alpha, alpha0);
-            fl += 1;
+            count(1);
             if (!(alpha <= cap)) return TB_STATUS_FACTORIZATION_FAILED;
         }
     }
     // dense.hpp:224-228 forward solve L b = rhs on F (column sweep == the
-    // reference's ascending row dot-form, element by element)
+    // reference's ascending row dot-form, element by element).  ldiag is 1
+    // outside F so every lane divides benign operands (no divergence).
+    __device__ __forceinline__ void trsv_fwd_step(int j, unsigned F, bool inF, double ldiag, double& s) {
+        const double q = s / ldiag;
+        const double bj = bcast(q, j);
+        if (lane == j) s = q;
+        else if (inF && lane > j) s -= L[lane + j * D] * bj;
+    }
     __device__ __forceinline__ double trsv_fwd(double b, unsigned F, double ldiag) {
         const bool inF = in_mask(F, lane);
-        double s = b;
+        double s = inF ? b : 0.0;
+        if (kUnroll) {
+#pragma unroll
+            for (int j = 0; j < D; ++j)
+                if (in_mask(F, j)) trsv_fwd_step(j, F, inF, ldiag, s);
+        } else {
 #pragma unroll 1
-        for (unsigned mj = F; mj; mj &= mj - 1) {
-            const int j = low_bit(mj);
-            if (lane == j) s = s / ldiag;
-            const double bj = bcast(s, j);
-            if (inF && lane > j) s -= L[lane + j * D] * bj;
+            for (unsigned mj = F; mj; mj &= mj - 1) trsv_fwd_step(low_bit(mj), F, inF, ldiag, s);
         }
         return s;
     }
     // dense.hpp:229-235 backward solve L^T b = rhs on F, exact order: for i
-    // descending, s = b_i - sum_{j > i ascending} L(j,i) b_j.
+    // descending, s = b_i - sum_{j > i ascending} L(j,i) b_j.  Every lane
+    // computes every b_i (redundantly, identical bits).
     __device__ __forceinline__ double trsv_bwd(double b, unsigned F) {
         double out = b;
-#pragma unroll 1
-        for (unsigned mi = F; mi; mi &= ~(1u << high_bit(mi))) {
-            const int i = high_bit(mi);
-            double s = bcast(b, i);
-#pragma unroll 1
-            for (unsigned mj = F & ~((2u << i) - 1u); mj; mj &= mj - 1) {
-                const int j = low_bit(mj);
-                s -= L[j + i * D] * bb[j];
+        if (kUnroll) {
+            double bv[D];
+#pragma unroll
+            for (int i = D - 1; i >= 0; --i) {
+                bv[i] = 0.0;
+                if (!in_mask(F, i)) continue;
+                double s = bcast(b, i);
+#pragma unroll
+                for (int j = i + 1; j < D; ++j)
+                    if (in_mask(F, j)) s -= L[j + i * D] * bv[j];
+                bv[i] = s / L[i + i * D];
+                if (lane == i) out = bv[i];
             }
-            const double bi = s / L[i + i * D];
-            if (lane == i) {
-                out = bi;
-                bb[i] = bi;
+        } else {
+            double* bb = s2 + tog;  // dedicated staging for this solve
+            tog ^= D;
+#pragma unroll 1
+            for (unsigned mi = F; mi; mi &= ~(1u << high_bit(mi))) {
+                const int i = high_bit(mi);
+                double s = bcast(b, i);
+#pragma unroll 1
+                for (unsigned mj = F & ~((2u << i) - 1u); mj; mj &= mj - 1) {
+                    const int j = low_bit(mj);
+                    s -= L[j + i * D] * bb[j];
+                }
+                const double bi = s / L[i + i * D];
+                if (lane == i) {
+                    out = bi;
+                    bb[i] = bi;
+                }
+                __syncwarp();
             }
-            __syncwarp();
         }
         return out;
     }
@@ -337,9 +409,9 @@ struct Warp {
                                               double& step, int& cg_status, int& iters) {
         const long long nf2 = (long long)nf * nf;
         double w = 0.0;
-        fl += nf;
+        count(nf);
         const double bhat = trsv_fwd(gfree * -1.0, F, ldiag);
-        fl += nf2;
+        count(nf2);
         const double bnorm = nrm2(bhat, F);
         iters = 0;
         if (bnorm == 0.0) {
@@ -356,14 +428,14 @@ struct Warp {
             const double z = trsv_bwd(p, F);
             double q = gemv(z, F);
             q = trsv_fwd(q, F, ldiag);
-            fl += 2 * nf2;
+            count(2 * nf2);
             const double ptq = dot(p, q, F);
             if (ptq <= 0.0) {
                 double sigma;
                 const int rc = trqsol(w, p, delta, F, sigma);
                 if (rc) return rc;
                 w += sigma * p;
-                fl += 2 * nf;
+                count(2 * nf);
                 cg_status = 2;
                 break;
             }
@@ -371,18 +443,18 @@ struct Warp {
             double sigma;
             const int rc = trqsol(w, p, delta, F, sigma);
             if (rc) return rc;
-            fl += 1;
+            count(1);
             if (alpha >= sigma) {
                 w += sigma * p;
-                fl += 2 * nf;
+                count(2 * nf);
                 cg_status = 1;
                 break;
             }
             w += alpha * p;
             r += (-alpha) * q;
-            fl += 4 * nf;
+            count(4 * nf);
             const double rtr = dot(r, r, F);
-            fl += 2;
+            count(2);
             if (sqrt(rtr) <= cfg->cg_tol * bnorm) {
                 cg_status = 0;
                 break;
@@ -390,11 +462,11 @@ struct Warp {
             const double beta = rtr / rho;  // tron.hpp:335 scal then axpy
             p = beta * p;
             p += 1.0 * r;
-            fl += 3 * nf + 1;
+            count(3 * nf + 1);
             rho = rtr;
         }
         step = trsv_bwd(w, F);
-        fl += nf2;
+        count(nf2);
         return 0;
     }
 
@@ -410,12 +482,12 @@ struct Warp {
             const double s = gpstep(x, beta, w, l, u, F);
             double gs;
             const double q = quad_model(g, s, F, gs);
-            fl += 2 * __popc(F) + 1;
+            count(2 * __popc(F) + 1);
             if (q <= cfg->mu0 * gs) search = false;
             else beta *= cfg->interp_factor;
         }
         if (beta < 1.0 && beta < bmin) beta = bmin;
-        fl += 2 * __popc(F);
+        count(2 * __popc(F));
         return clip(x + beta * w, l, u);
     }
 
@@ -428,7 +500,7 @@ struct Warp {
         const double extrap_factor = 1.0 / cfg->interp_factor;
         double alpha = alpha_start;
         const double mg = -1.0 * g;
-        fl += nn;
+        count(nn);
         double bmin, bmax;
         breakpt(x, mg, l, u, m, bmin, bmax);
         s = gpstep(x, -alpha, g, l, u, m);
@@ -439,7 +511,7 @@ struct Warp {
             double gs;
             const double q = quad_model(g, s, m, gs);
             if (!isfinite(q)) return TB_STATUS_EVALUATION_ERROR;
-            fl += 2 * nn + 1;
+            count(2 * nn + 1);
             interpolate = q >= cfg->mu0 * gs;
         }
         if (interpolate) {
@@ -452,7 +524,7 @@ struct Warp {
                     double gs;
                     const double q = quad_model(g, s, m, gs);
                     if (!isfinite(q)) return TB_STATUS_EVALUATION_ERROR;
-                    fl += 2 * nn + 1;
+                    count(2 * nn + 1);
                     search = q >= cfg->mu0 * gs;
                 }
             }
@@ -467,7 +539,7 @@ struct Warp {
                     double gs;
                     const double q = quad_model(g, s, m, gs);
                     if (!isfinite(q)) return TB_STATUS_EVALUATION_ERROR;
-                    fl += 2 * nn + 1;
+                    count(2 * nn + 1);
                     if (q < cfg->mu0 * gs) alpha_good = alpha;
                     else search = false;
                 } else {
@@ -487,9 +559,9 @@ struct Warp {
                                                  double& xout, double& sout, long long& cg_total) {
         const int nn = n;
         xout = clip(x0 + 1.0 * cs, l, u);
-        fl += 2 * nn;
+        count(2 * nn);
         double s = xout - x0;
-        fl += nn;
+        count(nn);
         double w = gemv(s, act);
         cg_total = 0;
 #pragma unroll 1
@@ -504,7 +576,7 @@ struct Warp {
             const double ldiag = fr ? L[lane + lane * D] : 1.0;
             if (__any_sync(FULL, fr && ldiag == 0.0)) return TB_STATUS_SINGULAR_FACTOR;
             const double gfree = w + g;
-            fl += nf;
+            count(nf);
             const double gfnorm = nrm2(g, F);
             double step;
             int cgs, its;
@@ -516,11 +588,11 @@ struct Warp {
                 s += xn - xout;
                 xout = xn;
             }
-            fl += 2 * nf;
+            count(2 * nf);
             w = gemv(s, act);
             const double t = w + g;
             const double gfnormf = seq_sum(t * t, F);
-            fl += 3 * nf + 2;
+            count(3 * nf + 2);
             if (sqrt(gfnormf) <= cfg->cg_tol * gfnorm) break;
             if (cgs == 1 || cgs == 3) break;
         }
@@ -536,12 +608,12 @@ struct Warp {
 // point of the most recent f evaluation (tron.hpp:474-476, 506, 532, 489),
 // so one context per point suffices.  Each value is produced by the same
 // tb_families.h expression as on the host.
-template <int FAM, int D>
+template <int FAM, int D, bool COUNT>
 struct DevFamily {
     double c0 = 0.0, c1 = 0.0, c2 = 0.0, c3 = 0.0;  // per-lane caches
     tb_branch_ctx* ctx = nullptr;
 
-    __device__ __forceinline__ void prepare(Warp<D>& W, double x) {
+    __device__ __forceinline__ void prepare(Warp<D, COUNT>& W, double x) {
         const int lane = W.lane, n = W.n;
         const bool act = lane < n;
         if (act) W.xs[lane] = x;
@@ -589,7 +661,7 @@ struct DevFamily {
             __syncwarp();
         }
     }
-    __device__ __forceinline__ double f(Warp<D>& W) {
+    __device__ __forceinline__ double f(Warp<D, COUNT>& W) {
         const int lane = W.lane, n = W.n;
         const double* prm = W.prm;
         if (FAM == TB_FAMILY_HS45) return tb_hs45_f(W.xs, n);
@@ -606,7 +678,7 @@ struct DevFamily {
         }
         return tb_br_f(ctx, prm, n);
     }
-    __device__ __forceinline__ double grad(Warp<D>& W) {
+    __device__ __forceinline__ double grad(Warp<D, COUNT>& W) {
         const int lane = W.lane, n = W.n;
         if (lane >= n) return 0.0;
         const double* prm = W.prm;
@@ -621,7 +693,7 @@ struct DevFamily {
         return tb_br_grad(ctx, n, lane);
     }
     // row `lane` of the Hessian into A[lane + j*D]
-    __device__ __forceinline__ void hess(Warp<D>& W) {
+    __device__ __forceinline__ void hess(Warp<D, COUNT>& W) {
         const int lane = W.lane, n = W.n;
         const double* prm = W.prm;
         if (lane < n) {
@@ -649,7 +721,7 @@ __device__ __forceinline__ unsigned long long globaltimer() {
 }
 
 // tron.hpp:453-549 solve(), one problem per warp (one warp per block).
-template <int FAM, int D>
+template <int FAM, int D, bool COUNT>
 __global__ void __launch_bounds__(32, 16) tron_solve_kernel(const __grid_constant__ KernelArgs a) {
     extern __shared__ double smem[];
     using SL = SmemLayout<D>;
@@ -657,11 +729,11 @@ __global__ void __launch_bounds__(32, 16) tron_solve_kernel(const __grid_constan
     if (pid >= a.count) return;
     const unsigned long long t_start = globaltimer();
 
-    Warp<D> W;
+    Warp<D, COUNT> W;
     W.A = smem + SL::A;
     W.L = smem + SL::L;
-    W.buf = smem + SL::BUF;
-    W.bb = smem + SL::BB;
+    W.s1 = smem + SL::S1;
+    W.s2 = smem + SL::S2;
     W.xs = smem + SL::XS;
     double* prm_s = smem + SL::PRM;
     W.n = a.n;
@@ -681,7 +753,7 @@ __global__ void __launch_bounds__(32, 16) tron_solve_kernel(const __grid_constan
         for (int k = lane; k < a.nparams; k += 32) prm_s[k] = gp[k];
     }
     W.prm = prm_s;
-    DevFamily<FAM, D> fam;
+    DevFamily<FAM, D, COUNT> fam;
     fam.ctx = reinterpret_cast<tb_branch_ctx*>(smem + SL::CTX);
     const double l = act ? a.lo[pid * n + lane] : 0.0;
     const double u = act ? a.up[pid * n + lane] : 0.0;
@@ -701,10 +773,10 @@ __global__ void __launch_bounds__(32, 16) tron_solve_kernel(const __grid_constan
         x = W.clip(x, l, u);
         fam.prepare(W, x);
         f = fam.f(W);
-        W.fl += tb_family_flops(FAM, n, 0);
+        W.count(tb_family_flops(FAM, n, 0));
         f_evals = 1;
         double g = fam.grad(W);
-        W.fl += tb_family_flops(FAM, n, 1);
+        W.count(tb_family_flops(FAM, n, 1));
         pg = W.pgnorm(x, g, l, u);
         double delta = cfg.has_delta0 ? cfg.delta0 : tb_smax(W.nrm2(g, W.act), 1.0);
         double alpha_c = 1.0;
@@ -717,7 +789,7 @@ __global__ void __launch_bounds__(32, 16) tron_solve_kernel(const __grid_constan
                 iterations = iter;
                 if (need_hessian) {  // family context holds the current x
                     fam.hess(W);
-                    W.fl += tb_family_flops(FAM, n, 2);
+                    W.count(tb_family_flops(FAM, n, 2));
                     need_hessian = false;
                 }
                 const long long fl_iter0 = W.fl;
@@ -740,17 +812,17 @@ __global__ void __launch_bounds__(32, 16) tron_solve_kernel(const __grid_constan
                 cg_iterations += cg_its;
                 fam.prepare(W, xt);
                 const double f_trial = fam.f(W);
-                W.fl += tb_family_flops(FAM, n, 0);
+                W.count(tb_family_flops(FAM, n, 0));
                 ++f_evals;
 
                 const double as = W.gemv(s, W.act);
                 double gs, sas, snn;
                 W.seq_sum3(g * s, s * as, s * s, W.act, gs, sas, snn);
-                W.fl += 6 * n + 1;
+                W.count(6 * n + 1);
                 const double prered = -(gs + 0.5 * sas);
                 const double actred = f - f_trial;
                 const double snorm = sqrt(snn);
-                W.fl += 4;
+                W.count(4);
                 if (iter == 1) delta = tb_smin(delta, snorm);
 
                 double alphax;
@@ -766,14 +838,14 @@ __global__ void __launch_bounds__(32, 16) tron_solve_kernel(const __grid_constan
                 else
                     delta = tb_smax(delta, tb_smin(alphax * snorm, cfg.sigma3 * delta));
                 delta = tb_smin(delta, cfg.delta_max);
-                W.fl += 12;
+                W.count(12);
 
                 const bool accepted = actred > cfg.eta0 * prered;
                 if (accepted) {
                     x = xt;
                     f = f_trial;
                     g = fam.grad(W);  // context was prepared at xt
-                    W.fl += tb_family_flops(FAM, n, 1);
+                    W.count(tb_family_flops(FAM, n, 1));
                     need_hessian = true;
                     pg = W.pgnorm(x, g, l, u);
                     if (pg <= cfg.tol_pg) {
@@ -791,7 +863,7 @@ __global__ void __launch_bounds__(32, 16) tron_solve_kernel(const __grid_constan
                     const long long rem = cfg.max_iter - iter;
                     cg_iterations += rem * cg_its;
                     f_evals += rem;
-                    W.fl += rem * (W.fl - fl_iter0);
+                    W.count(rem * (W.fl - fl_iter0));
                     iterations = cfg.max_iter;
                     break;
                 }

@@ -4,6 +4,9 @@
 
 namespace tbdev {
 struct KernelArgs;
+}
+#include "tron_device.cuh"
+namespace tbdev {
 cudaError_t launch_tron(int family, const KernelArgs& a, cudaStream_t st);
 int max_warp_dim();
 }  // namespace tbdev

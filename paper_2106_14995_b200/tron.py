@@ -207,8 +207,10 @@ class Solver:
             pass
 
     def solve_batch(self, problems: ProblemBatch, x0s=None, cfg: TronConfig = TronConfig(),
-                    out: Optional[BatchResult] = None, stream=None) -> BatchResult:
-        """batch.hpp:27-78.  x0s defaults to problems.x0."""
+                    out: Optional[BatchResult] = None, stream=None, count_flops: bool = False) -> BatchResult:
+        """batch.hpp:27-78.  x0s defaults to problems.x0.  count_flops selects
+        the kernel variant that also counts algorithmic flops per problem
+        (out.flops); results are identical either way."""
         x0s = problems.x0 if x0s is None else x0s
         if x0s is None:
             raise ValueError("solve_batch: no starting points")
@@ -236,7 +238,7 @@ class Solver:
         r.x_star, r.f_star, r.pg_norm = _ptr(out.x_star), _ptr(out.f_star), _ptr(out.pg_norm)
         r.status, r.iterations = _ptr(out.status), _ptr(out.iterations)
         r.cg_iterations, r.f_evals = _ptr(out.cg_iterations), _ptr(out.f_evals)
-        r.wall_time, r.flops = _ptr(out.per_problem_time), _ptr(out.flops)
+        r.wall_time, r.flops = _ptr(out.per_problem_time), (_ptr(out.flops) if count_flops else 0)
         r.memspace = L.TB_MEM_DEVICE if _is_device(out.status) else L.TB_MEM_HOST
         c = cfg.to_c()
         if stream is not None:

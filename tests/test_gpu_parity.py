@@ -14,10 +14,12 @@ pytestmark = pytest.mark.gpu
 def test_ncvx_bitwise(solver, d):
     n = 1024 if d <= 8 else 128
     b = synth.ncvx(n, d, seed=3 + d)
-    res = solver.solve_batch(b)
+    res = solver.solve_batch(b, count_flops=True)
     ref = po.solve_batch(b, impl="oracle", workers=8)
     assert_bitwise(res, ref, label=f"ncvx d={d}")
     assert np.array_equal(host(res.flops), ref.flops)
+    plain = solver.solve_batch(b)  # non-counting kernel variant: same results
+    assert_bitwise(plain, ref, label=f"ncvx d={d} (no count)")
 
 
 def test_c1_ncvx_d4_1024(solver):
@@ -32,7 +34,7 @@ def test_c1_ncvx_d4_1024(solver):
 @pytest.mark.parametrize("dim", [4, 6])
 def test_branch_bitwise(solver, dim):
     b = synth.branch(8192, dim, seed=2)
-    res = solver.solve_batch(b)
+    res = solver.solve_batch(b, count_flops=True)
     ref = po.solve_batch(b, impl="oracle", workers=8)
     assert_bitwise(res, ref, label=f"branch{dim}")
     assert np.array_equal(host(res.flops), ref.flops)
@@ -176,8 +178,8 @@ def test_invalid_bounds_raise(solver):
 
 def test_fast_forward_on_device_is_neutral():
     b = synth.branch(8192, 6, seed=5)
-    a = Solver((0,), fast_forward=True).solve_batch(b)
-    z = Solver((0,), fast_forward=False).solve_batch(b)
+    a = Solver((0,), fast_forward=True).solve_batch(b, count_flops=True)
+    z = Solver((0,), fast_forward=False).solve_batch(b, count_flops=True)
     assert_bitwise(a, z, label="device ff")
     assert np.array_equal(host(a.flops), host(z.flops))
 
