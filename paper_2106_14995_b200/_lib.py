@@ -9,7 +9,7 @@ import ctypes as C
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libtronbatch_b200.so")
+LIB_PATH = os.environ.get("TB_LIB_PATH") or os.path.join(_HERE, "libtronbatch_b200.so")
 
 TB_OK = 0
 TB_E_INVALID_ARGUMENT = 1

@@ -34,7 +34,25 @@
 #include "tb_families.h"
 #include "tb_flops.h"
 
+#ifndef TB_MIN_BLOCKS
+#define TB_MIN_BLOCKS 16  // resident one-warp blocks per SM the register budget targets
+#endif
+
+// Debug build only (-DTB_PHASES): per-phase clock64() accumulation, read back
+// with tb_debug_read_phases() (scripts/phase_profile.py).
+#ifdef TB_PHASES
+#define TB_PH_BEGIN(k) const long long tb_ph_t0_##k = clock64();
+#define TB_PH_END(w, k) (w).ph[k] += clock64() - tb_ph_t0_##k;
+#else
+#define TB_PH_BEGIN(k)
+#define TB_PH_END(w, k)
+#endif
+
 namespace tbdev {
+
+#ifdef TB_PHASES
+__device__ unsigned long long g_phase_cycles[8];
+#endif
 
 constexpr unsigned FULL = 0xffffffffu;
 
@@ -83,9 +101,11 @@ struct KernelArgs {
 // shared memory per warp (doubles; every region starts at an even offset)
 template <int D>
 struct SmemLayout {
-    static constexpr int A = 0;              // D*D Hessian
-    static constexpr int L = A + D * D;      // D*D factor
-    static constexpr int S1 = L + D * D;     // 2*D ordered-sum staging (double buffered)
+    static constexpr int GS = D <= 4 ? 4 : (D <= 8 ? 8 : (D <= 16 ? 16 : 32));
+    static constexpr int A = 0;                      // D*D Hessian
+    static constexpr int L = A + D * D;              // (32/GS)*D*D factors, one per lane group
+    static constexpr int RD = L + (32 / GS) * D * D; // D reciprocal diagonal of the winning factor
+    static constexpr int S1 = RD + D;                // 2*D ordered-sum staging (double buffered)
     static constexpr int S2 = S1 + 2 * D;    // 2*D second staging (double buffered)
     static constexpr int XS = S2 + 2 * D;    // D point for family evaluations
     static constexpr int CTX = XS + D;       // family context (branch: sizeof(tb_branch_ctx))
@@ -100,7 +120,9 @@ template <int D, bool COUNT>
 struct Warp {
     static constexpr bool kUnroll = D <= 8;
     double* A;
-    double* L;
+    double* L;   // G*D*D: one factor per lane group (parallel shift attempts)
+    double* Lw;  // the successful attempt's factor
+    double* RD;  // D: RN(1 / L(i,i)) of Lw
     double* s1;  // 2*D
     double* s2;  // 2*D
     double* xs;  // D
@@ -111,6 +133,10 @@ struct Warp {
     int tog;        // staging toggle (0 or D)
     unsigned act;   // lanes 0..n-1
     long long fl;   // algorithmic flop counter (tb_flops.h model), COUNT builds only
+    double extrap;  // 1.0 / cfg->interp_factor
+#ifdef TB_PHASES
+    long long ph[8];
+#endif
 
     __device__ __forceinline__ void count(long long v) {
         if (COUNT) fl += v;
@@ -254,65 +280,81 @@ struct Warp {
     }
 
     // ------------------------------------------------ dense.hpp factorization
-    // one column of dense.hpp:141-154 (left-looking, zero-skip on L(j,k),
-    // pivot test !(pivot > 0), division by sqrt(pivot))
-    __device__ __forceinline__ bool chol_column(unsigned F, int j, double shift, int rem) {
-        const bool row = in_mask(F, lane) && lane >= j;
-        double lij = row ? A[lane + j * D] : 0.0;
-        if (lane == j) lij += shift;
-        long long cnt = 0;
+    // Shift escalation in parallel (dense.hpp:182-201).  The reference tries
+    // A + a_k I for a_0 = 0, a_{k+1} = max(2 a_k, alpha0), k = 0, 1, ...
+    // sequentially until one factorization succeeds (cap -> failure).  Every
+    // attempt is an independent function of (A[F,F], a_k), so G lane groups of
+    // GS >= D lanes each run attempts k0 .. k0+G-1 at once; the first success
+    // in k order is the reference's result (same L, same shift, same flop
+    // count).  Within a group, lane i owns row i of the current column
+    // (left-looking, dense.hpp:141-154: zero-skip on L(j,k), pivot test
+    // !(pivot > 0), division by sqrt(pivot)).
+    static constexpr int GS = D <= 4 ? 4 : (D <= 8 ? 8 : (D <= 16 ? 16 : 32));
+    static constexpr int G = 32 / GS;
+
+    // one round of G attempts; returns the winning group or -1.  `fl_round`
+    // receives the flops the reference spends on the attempts up to and
+    // including the winner (all G if none wins).
+    __device__ __forceinline__ int chol_round(unsigned F, int nf, double sh, bool valid, long long& fl_round) {
+        const int g = lane / GS, i = lane % GS;
+        double* Lg = L + g * D * D;
+        const bool inF = i < D && in_mask(F, i);
+        bool alive = valid;
+        int rem = nf;
+        int my_fl = 0;  // flops of this group's attempt (counted on lane i == 0)
+        auto column = [&](int j) {
+            const bool row = alive && inF && i >= j;
+            double lij = row ? A[i + j * D] : 0.0;
+            if (i == j) lij += sh;
+            int cnt = 0;
+            auto kstep = [&](int k) {
+                const double ljk = Lg[j + k * D];
+                const bool nz = ljk != 0.0;
+                if (nz && row) lij -= ljk * Lg[i + k * D];
+                cnt += nz;
+            };
+            if (kUnroll) {
+#pragma unroll
+                for (int k = 0; k < D - 1; ++k)
+                    if (k < j && in_mask(F, k)) kstep(k);
+            } else {
+#pragma unroll 1
+                for (unsigned mk = F & ((1u << j) - 1u); mk; mk &= mk - 1) kstep(low_bit(mk));
+            }
+            const double pivot = __shfl_sync(FULL, lij, j, GS);
+            const bool ok = pivot > 0.0;
+            if (alive) my_fl += 1 + 2 * rem * cnt + (ok ? rem : 0);
+            const double d = sqrt(ok ? pivot : 1.0);
+            const double q = lij / d;
+            if (row && ok) Lg[i + j * D] = i == j ? d : q;
+            alive = alive && ok;
+            --rem;
+            __syncwarp();
+        };
         if (kUnroll) {
 #pragma unroll
-            for (int k = 0; k < D - 1; ++k) {
-                if (k >= j || !in_mask(F, k)) continue;
-                const double ljk = L[j + k * D];
-                if (ljk == 0.0) continue;
-                if (row) lij -= ljk * L[lane + k * D];
-                ++cnt;
-            }
+            for (int j = 0; j < D; ++j)
+                if (in_mask(F, j) && __any_sync(FULL, alive)) column(j);
         } else {
 #pragma unroll 1
-            for (unsigned mk = F & ((1u << j) - 1u); mk; mk &= mk - 1) {
-                const int k = low_bit(mk);
-                const double ljk = L[j + k * D];
-                if (ljk == 0.0) continue;
-                if (row) lij -= ljk * L[lane + k * D];
-                ++cnt;
-            }
+            for (unsigned mj = F; mj && __any_sync(FULL, alive); mj &= mj - 1) column(low_bit(mj));
         }
-        count(1 + 2LL * rem * cnt);
-        const double pivot = bcast(lij, j);
-        if (!(pivot > 0.0)) return false;
-        const double d = sqrt(pivot);
-        const double q = lij / d;  // every lane (non-rows hold 0): no divergence
-        lij = lane == j ? d : q;
-        if (row) L[lane + j * D] = lij;
-        count(rem);  // sqrt + (rem - 1) divisions
-        __syncwarp();
-        return true;
-    }
-    __device__ __forceinline__ bool chol_left(unsigned F, int nf, double shift) {
-        int rem = nf;  // free rows at or below the current column
-        if (kUnroll) {
-#pragma unroll
-            for (int j = 0; j < D; ++j) {
-                if (!in_mask(F, j)) continue;
-                if (!chol_column(F, j, shift, rem)) return false;
-                --rem;
-            }
-        } else {
-#pragma unroll 1
-            for (unsigned mj = F; mj; mj &= mj - 1) {
-                if (!chol_column(F, low_bit(mj), shift, rem)) return false;
-                --rem;
-            }
+        const unsigned wins = __ballot_sync(FULL, i == 0 && alive);
+        const int winner = wins ? low_bit(wins) / GS : -1;
+        if (COUNT) {
+            const int last = winner >= 0 ? winner : G - 1;
+            // failed attempts also pay the alpha update (dense.hpp:197)
+            const int contrib = (i == 0 && valid && g <= last) ? my_fl + (g < winner || winner < 0 ? 1 : 0) : 0;
+            fl_round = __reduce_add_sync(FULL, (unsigned)contrib);
         }
-        return true;
+        return winner;
     }
-    // dense.hpp:182-201 shifted_factorize.  Returns 0 or
+
+    // dense.hpp:182-201 shifted_factorize on A[F,F].  On success Lw points at
+    // the factor and RD holds RN(1 / L(i,i)).  Returns 0 or
     // TB_STATUS_FACTORIZATION_FAILED.
     __device__ __forceinline__ int ccf(unsigned F, int nf, double& shift) {
-        const bool inF = in_mask(F, lane);
+        const bool inF = lane < D && in_mask(F, lane);
         double dg = inF ? fabs(A[lane + lane * D]) : 0.0;
         if (isnan(dg)) dg = 0.0;
         double ma = 0.0;
@@ -327,37 +369,67 @@ struct Warp {
         const double max_abs = warp_max_nonneg(ma);
         const double alpha0 = tb_smax(1e-3 * max_diag, 1e-8);
         const double cap = 1e8 * tb_smax(1.0, max_abs);
-        double alpha = 0.0;
+        const int g = lane / GS;
+        double base = 0.0;  // a_{k0}
 #pragma unroll 1
-        for (;;) {
-            if (chol_left(F, nf, alpha)) {
-                shift = alpha;
+        for (int k0 = 0; k0 < 4096; k0 += G) {
+            double sh = base;
+            for (int t = 0; t < g; ++t) sh = tb_smax(2.0 * sh, alpha0);
+            const bool valid = (k0 + g == 0) || (sh <= cap);
+            long long flr = 0;
+            const int w = chol_round(F, nf, sh, valid, flr);
+            count(flr);
+            if (w >= 0) {
+                shift = __shfl_sync(FULL, sh, w * GS);
+                Lw = L + w * D * D;
+                if (lane < D) {
+                    const double dii = Lw[lane + lane * D];
+                    RD[lane] = inF ? 1.0 / dii : 1.0;
+                }
+                __syncwarp();
                 return 0;
             }
-            alpha = tb_smax(2.0 * alpha, alpha0);
-            count(1);
-            if (!(alpha <= cap)) return TB_STATUS_FACTORIZATION_FAILED;
+            // no success among attempts k0..k0+G-1: the reference throws at
+            // the first a_k > cap (all earlier attempts failed)
+            if (!__all_sync(FULL, valid)) return TB_STATUS_FACTORIZATION_FAILED;
+            for (int t = 0; t < G; ++t) base = tb_smax(2.0 * base, alpha0);
         }
+        // unreachable for finite data (alpha doubles past any finite cap);
+        // with an infinite cap the reference never terminates
+        return TB_STATUS_FACTORIZATION_FAILED;
     }
+
+    // correctly rounded a / d from r = RN(1/d) (Markstein): q0 = RN(a r),
+    // e = a - d q0 exactly (FMA), RN(q0 + e r) == RN(a / d) when no
+    // intermediate is subnormal / huge; zero, subnormal, huge, inf and NaN
+    // quotients take the IEEE division.  3 dependent ops instead of ~15.
+    __device__ __forceinline__ double div_rcp(double a, double d, double r) const {
+        const double q0 = a * r;
+        const unsigned ex = ((unsigned)__double2hiint(q0) >> 20) & 0x7FFu;
+        if (ex - 64u > 1918u) return a / d;
+        const double e = fma(-q0, d, a);
+        return fma(e, r, q0);
+    }
+
     // dense.hpp:224-228 forward solve L b = rhs on F (column sweep == the
-    // reference's ascending row dot-form, element by element).  ldiag is 1
-    // outside F so every lane divides benign operands (no divergence).
-    __device__ __forceinline__ void trsv_fwd_step(int j, unsigned F, bool inF, double ldiag, double& s) {
-        const double q = s / ldiag;
-        const double bj = bcast(q, j);
+    // reference's ascending row dot-form, element by element); every lane
+    // divides (benign operands outside F), lane j's quotient is broadcast.
+    __device__ __forceinline__ void trsv_fwd_step(int j, bool inF, double& s) {
+        // every lane divides lane j's value (uniform operands: no divergence)
+        const double q = div_rcp(bcast(s, j), Lw[j + j * D], RD[j]);
         if (lane == j) s = q;
-        else if (inF && lane > j) s -= L[lane + j * D] * bj;
+        else if (inF && lane > j) s -= Lw[lane + j * D] * q;
     }
-    __device__ __forceinline__ double trsv_fwd(double b, unsigned F, double ldiag) {
-        const bool inF = in_mask(F, lane);
+    __device__ __forceinline__ double trsv_fwd(double b, unsigned F, double ldiag, double rdiag) {
+        const bool inF = lane < D && in_mask(F, lane);
         double s = inF ? b : 0.0;
         if (kUnroll) {
 #pragma unroll
             for (int j = 0; j < D; ++j)
-                if (in_mask(F, j)) trsv_fwd_step(j, F, inF, ldiag, s);
+                if (in_mask(F, j)) trsv_fwd_step(j, inF, s);
         } else {
 #pragma unroll 1
-            for (unsigned mj = F; mj; mj &= mj - 1) trsv_fwd_step(low_bit(mj), F, inF, ldiag, s);
+            for (unsigned mj = F; mj; mj &= mj - 1) trsv_fwd_step(low_bit(mj), inF, s);
         }
         return s;
     }
@@ -375,8 +447,8 @@ struct Warp {
                 double s = bcast(b, i);
 #pragma unroll
                 for (int j = i + 1; j < D; ++j)
-                    if (in_mask(F, j)) s -= L[j + i * D] * bv[j];
-                bv[i] = s / L[i + i * D];
+                    if (in_mask(F, j)) s -= Lw[j + i * D] * bv[j];
+                bv[i] = div_rcp(s, Lw[i + i * D], RD[i]);
                 if (lane == i) out = bv[i];
             }
         } else {
@@ -389,9 +461,9 @@ struct Warp {
 #pragma unroll 1
                 for (unsigned mj = F & ~((2u << i) - 1u); mj; mj &= mj - 1) {
                     const int j = low_bit(mj);
-                    s -= L[j + i * D] * bb[j];
+                    s -= Lw[j + i * D] * bb[j];
                 }
-                const double bi = s / L[i + i * D];
+                const double bi = div_rcp(s, Lw[i + i * D], RD[i]);
                 if (lane == i) {
                     out = bi;
                     bb[i] = bi;
@@ -406,11 +478,11 @@ struct Warp {
     // Steihaug PCG on the free set.  Returns 0 or an error status.
     // cg_status: 0 Converged, 1 Boundary, 2 NegCurve, 3 IterCap
     __device__ __forceinline__ int precond_cg(unsigned F, int nf, double gfree, double delta, double ldiag,
-                                              double& step, int& cg_status, int& iters) {
+                                              double rdiag, double& step, int& cg_status, int& iters) {
         const long long nf2 = (long long)nf * nf;
         double w = 0.0;
         count(nf);
-        const double bhat = trsv_fwd(gfree * -1.0, F, ldiag);
+        const double bhat = trsv_fwd(gfree * -1.0, F, ldiag, rdiag);
         count(nf2);
         const double bnorm = nrm2(bhat, F);
         iters = 0;
@@ -427,7 +499,7 @@ struct Warp {
             iters = k;
             const double z = trsv_bwd(p, F);
             double q = gemv(z, F);
-            q = trsv_fwd(q, F, ldiag);
+            q = trsv_fwd(q, F, ldiag, rdiag);
             count(2 * nf2);
             const double ptq = dot(p, q, F);
             if (ptq <= 0.0) {
@@ -497,7 +569,7 @@ struct Warp {
         const unsigned m = act;
         const int nn = n;
         const double radius = cfg->mu1 * delta;
-        const double extrap_factor = 1.0 / cfg->interp_factor;
+        const double extrap_factor = extrap;  // 1.0 / interp_factor (tron.hpp:204), once per solve
         double alpha = alpha_start;
         const double mg = -1.0 * g;
         count(nn);
@@ -571,19 +643,26 @@ struct Warp {
             const int nf = __popc(F);
             if (nf == 0) break;
             double shift;
+            TB_PH_BEGIN(2)
             int rc = ccf(F, nf, shift);
+            TB_PH_END(*this, 2)
             if (rc) return rc;
-            const double ldiag = fr ? L[lane + lane * D] : 1.0;
+            const double ldiag = fr ? Lw[lane + lane * D] : 1.0;
+            const double rdiag = fr ? RD[lane] : 1.0;
             if (__any_sync(FULL, fr && ldiag == 0.0)) return TB_STATUS_SINGULAR_FACTOR;
             const double gfree = w + g;
             count(nf);
             const double gfnorm = nrm2(g, F);
             double step;
             int cgs, its;
-            rc = precond_cg(F, nf, gfree, delta, ldiag, step, cgs, its);
+            TB_PH_BEGIN(3)
+            rc = precond_cg(F, nf, gfree, delta, ldiag, rdiag, step, cgs, its);
+            TB_PH_END(*this, 3)
             if (rc) return rc;
             cg_total += its;
+            TB_PH_BEGIN(4)
             const double xn = line_search(xout, l, u, gfree, step, F);
+            TB_PH_END(*this, 4)
             if (fr) {
                 s += xn - xout;
                 xout = xn;
@@ -706,8 +785,20 @@ struct DevFamily {
                 const double* a = k + n;
                 for (int j = 0; j < n; ++j) W.A[lane + j * D] = tb_ncvx_H(prm, n, lane, j);
                 W.A[lane + lane * D] = (W.A[lane + lane * D] + (3.0 * k[lane]) * (c0 * c0)) - a[lane] * c2;
-            } else {
-                for (int j = 0; j < n; ++j) W.A[lane + j * D] = tb_br_hess(ctx, prm, n, lane, j);
+            }
+        }
+        if (FAM == TB_FAMILY_BRANCH) {
+            // one lower-triangle entry per lane (n(n+1)/2 <= 21 entries);
+            // tb_br_hess canonicalises (i, j) so both halves get the same bits
+            int a = 0, b = lane;
+            while (b > a) {
+                b -= a + 1;
+                ++a;
+            }
+            if (a < n) {
+                const double h = tb_br_hess(ctx, prm, n, a, b);
+                W.A[a + b * D] = h;
+                W.A[b + a * D] = h;
             }
         }
         __syncwarp();
@@ -722,7 +813,7 @@ __device__ __forceinline__ unsigned long long globaltimer() {
 
 // tron.hpp:453-549 solve(), one problem per warp (one warp per block).
 template <int FAM, int D, bool COUNT>
-__global__ void __launch_bounds__(32, 16) tron_solve_kernel(const __grid_constant__ KernelArgs a) {
+__global__ void __launch_bounds__(32, TB_MIN_BLOCKS) tron_solve_kernel(const __grid_constant__ KernelArgs a) {
     extern __shared__ double smem[];
     using SL = SmemLayout<D>;
     const long long pid = blockIdx.x;
@@ -732,6 +823,8 @@ __global__ void __launch_bounds__(32, 16) tron_solve_kernel(const __grid_constan
     Warp<D, COUNT> W;
     W.A = smem + SL::A;
     W.L = smem + SL::L;
+    W.Lw = W.L;
+    W.RD = smem + SL::RD;
     W.s1 = smem + SL::S1;
     W.s2 = smem + SL::S2;
     W.xs = smem + SL::XS;
@@ -741,7 +834,12 @@ __global__ void __launch_bounds__(32, 16) tron_solve_kernel(const __grid_constan
     W.tog = 0;
     W.act = (a.n >= 32) ? FULL : ((1u << a.n) - 1u);
     W.fl = 0;
+#ifdef TB_PHASES
+    for (int k = 0; k < 8; ++k) W.ph[k] = 0;
+    const long long tb_ph_total0 = clock64();
+#endif
     W.cfg = &a.cfg;
+    W.extrap = 1.0 / a.cfg.interp_factor;
     const int n = a.n;
     const int lane = W.lane;
     const bool act = lane < n;
@@ -788,7 +886,9 @@ __global__ void __launch_bounds__(32, 16) tron_solve_kernel(const __grid_constan
             for (int iter = 1; iter <= cfg.max_iter; ++iter) {
                 iterations = iter;
                 if (need_hessian) {  // family context holds the current x
+                    TB_PH_BEGIN(0)
                     fam.hess(W);
+                    TB_PH_END(W, 0)
                     W.count(tb_family_flops(FAM, n, 2));
                     need_hessian = false;
                 }
@@ -796,7 +896,9 @@ __global__ void __launch_bounds__(32, 16) tron_solve_kernel(const __grid_constan
                 const double delta_in = delta, alpha_in = alpha_c;
 
                 double cs, alpha_new;
+                TB_PH_BEGIN(1)
                 int rc = W.cauchy(x, g, l, u, delta, alpha_c, alpha_new, cs);
+                TB_PH_END(W, 1)
                 if (rc) {
                     status = rc;
                     break;
@@ -804,17 +906,21 @@ __global__ void __launch_bounds__(32, 16) tron_solve_kernel(const __grid_constan
                 alpha_c = alpha_new;
                 double xt, s;
                 long long cg_its;
+                TB_PH_BEGIN(5)
                 rc = W.subspace_step(x, g, l, u, delta, cs, xt, s, cg_its);
+                TB_PH_END(W, 5)
                 if (rc) {
                     status = rc;  // FactorizationFailed caught like tron.hpp:499-501
                     break;
                 }
                 cg_iterations += cg_its;
+                TB_PH_BEGIN(6)
                 fam.prepare(W, xt);
                 const double f_trial = fam.f(W);
                 W.count(tb_family_flops(FAM, n, 0));
                 ++f_evals;
 
+                TB_PH_END(W, 6)
                 const double as = W.gemv(s, W.act);
                 double gs, sas, snn;
                 W.seq_sum3(g * s, s * as, s * s, W.act, gs, sas, snn);
@@ -871,6 +977,11 @@ __global__ void __launch_bounds__(32, 16) tron_solve_kernel(const __grid_constan
         }
     }
 
+#ifdef TB_PHASES
+    W.ph[7] = clock64() - tb_ph_total0;
+    if (lane == 0)
+        for (int k = 0; k < 8; ++k) atomicAdd(&g_phase_cycles[k], (unsigned long long)W.ph[k]);
+#endif
     if (act && a.x_star) a.x_star[pid * n + lane] = x;
     if (lane == 0) {
         if (a.f_star) a.f_star[pid] = f;
