@@ -34,6 +34,17 @@
 #include "tb_families.h"
 #include "tb_flops.h"
 
+#ifndef TB_UNROLL_MAX
+#define TB_UNROLL_MAX 8  // fully unroll the D-loops of kernels with D <= this
+#endif
+#ifndef TB_OUTLINE_SOLVES
+#define TB_OUTLINE_SOLVES 0  // 1: one out-of-line copy of each triangular solve (measured slower)
+#endif
+#if TB_OUTLINE_SOLVES
+#define TB_SOLVE_INLINE __noinline__
+#else
+#define TB_SOLVE_INLINE __forceinline__
+#endif
 #ifndef TB_MIN_BLOCKS
 #define TB_MIN_BLOCKS 16  // resident one-warp blocks per SM the register budget targets
 #endif
@@ -60,6 +71,10 @@ __device__ __forceinline__ int lane_id() { return threadIdx.x & 31; }
 __device__ __forceinline__ bool in_mask(unsigned m, int i) { return (m >> i) & 1u; }
 __device__ __forceinline__ int low_bit(unsigned m) { return __ffs(m) - 1; }
 __device__ __forceinline__ int high_bit(unsigned m) { return 31 - __clz(m); }
+
+// IEEE division kept out of line for rare paths (code size: the kernel's hot
+// loop must stay small for the instruction cache).
+static __device__ __noinline__ double div_ieee(double a, double d) { return a / d; }
 
 // max / min over the warp of NON-NEGATIVE doubles (+0.0 .. +inf, no NaN):
 // IEEE bit patterns of such values order like unsigned integers.
@@ -115,10 +130,88 @@ struct SmemLayout {
     static_assert(D % 2 == 0, "D must be even (16-byte staging loads)");
 };
 
+// ------------------------------------------------------------ solves
+// Correctly rounded a / d from r = RN(1/d) (Markstein): q0 = RN(a r),
+// e = a - d q0 exactly (FMA), RN(q0 + e r) == RN(a / d) when no intermediate
+// is subnormal / huge; zero, subnormal, huge, inf and NaN quotients take the
+// IEEE division.  3 dependent ops instead of ~15 (DDIV ~125 cycles).
+__device__ __forceinline__ double div_rcp(double a, double d, double r) {
+    const double q0 = a * r;
+    const unsigned ex = ((unsigned)__double2hiint(q0) >> 20) & 0x7FFu;
+    if (ex - 64u > 1918u) return div_ieee(a, d);
+    const double e = fma(-q0, d, a);
+    return fma(e, r, q0);
+}
+
+// dense.hpp:224-228 forward solve L b = rhs on F (column sweep == the
+// reference's ascending row dot-form, element by element); lane j's value is
+// broadcast and every lane divides it (uniform operands, no divergence).
+template <int D, bool UNROLL>
+__device__ TB_SOLVE_INLINE double trsv_fwd_fn(const double* __restrict__ Lw, const double* __restrict__ RD, double b,
+                                             unsigned F, int lane) {
+    const bool inF = lane < D && in_mask(F, lane);
+    double s = inF ? b : 0.0;
+    auto step = [&](int j) {
+        const double q = div_rcp(__shfl_sync(FULL, s, j), Lw[j + j * D], RD[j]);
+        if (lane == j) s = q;
+        else if (inF && lane > j) s -= Lw[lane + j * D] * q;
+    };
+    if (UNROLL) {
+#pragma unroll
+        for (int j = 0; j < D; ++j)
+            if (in_mask(F, j)) step(j);
+    } else {
+#pragma unroll 1
+        for (unsigned mj = F; mj; mj &= mj - 1) step(low_bit(mj));
+    }
+    return s;
+}
+
+// dense.hpp:229-235 backward solve L^T b = rhs on F, exact order: for i
+// descending, s = b_i - sum_{j > i ascending} L(j,i) b_j.  Every lane computes
+// every b_i (redundantly, identical bits); bb is D doubles of staging.
+template <int D, bool UNROLL>
+__device__ TB_SOLVE_INLINE double trsv_bwd_fn(const double* __restrict__ Lw, const double* __restrict__ RD,
+                                             double* __restrict__ bb, double b, unsigned F, int lane) {
+    double out = b;
+    if (UNROLL) {
+        double bv[D];
+#pragma unroll
+        for (int i = D - 1; i >= 0; --i) {
+            bv[i] = 0.0;
+            if (!in_mask(F, i)) continue;
+            double s = __shfl_sync(FULL, b, i);
+#pragma unroll
+            for (int j = i + 1; j < D; ++j)
+                if (in_mask(F, j)) s -= Lw[j + i * D] * bv[j];
+            bv[i] = div_rcp(s, Lw[i + i * D], RD[i]);
+            if (lane == i) out = bv[i];
+        }
+    } else {
+#pragma unroll 1
+        for (unsigned mi = F; mi; mi &= ~(1u << high_bit(mi))) {
+            const int i = high_bit(mi);
+            double s = __shfl_sync(FULL, b, i);
+#pragma unroll 1
+            for (unsigned mj = F & ~((2u << i) - 1u); mj; mj &= mj - 1) {
+                const int j = low_bit(mj);
+                s -= Lw[j + i * D] * bb[j];
+            }
+            const double bi = div_rcp(s, Lw[i + i * D], RD[i]);
+            if (lane == i) {
+                out = bi;
+                bb[i] = bi;
+            }
+            __syncwarp();
+        }
+    }
+    return out;
+}
+
 // ---------------------------------------------------------------- per warp
 template <int D, bool COUNT>
 struct Warp {
-    static constexpr bool kUnroll = D <= 8;
+    static constexpr bool kUnroll = D <= TB_UNROLL_MAX;
     double* A;
     double* L;   // G*D*D: one factor per lane group (parallel shift attempts)
     double* Lw;  // the successful attempt's factor
@@ -399,79 +492,13 @@ struct Warp {
         return TB_STATUS_FACTORIZATION_FAILED;
     }
 
-    // correctly rounded a / d from r = RN(1/d) (Markstein): q0 = RN(a r),
-    // e = a - d q0 exactly (FMA), RN(q0 + e r) == RN(a / d) when no
-    // intermediate is subnormal / huge; zero, subnormal, huge, inf and NaN
-    // quotients take the IEEE division.  3 dependent ops instead of ~15.
-    __device__ __forceinline__ double div_rcp(double a, double d, double r) const {
-        const double q0 = a * r;
-        const unsigned ex = ((unsigned)__double2hiint(q0) >> 20) & 0x7FFu;
-        if (ex - 64u > 1918u) return a / d;
-        const double e = fma(-q0, d, a);
-        return fma(e, r, q0);
+    __device__ __forceinline__ double trsv_fwd(double b, unsigned F, double, double) {
+        return trsv_fwd_fn<D, kUnroll>(Lw, RD, b, F, lane);
     }
-
-    // dense.hpp:224-228 forward solve L b = rhs on F (column sweep == the
-    // reference's ascending row dot-form, element by element); every lane
-    // divides (benign operands outside F), lane j's quotient is broadcast.
-    __device__ __forceinline__ void trsv_fwd_step(int j, bool inF, double& s) {
-        // every lane divides lane j's value (uniform operands: no divergence)
-        const double q = div_rcp(bcast(s, j), Lw[j + j * D], RD[j]);
-        if (lane == j) s = q;
-        else if (inF && lane > j) s -= Lw[lane + j * D] * q;
-    }
-    __device__ __forceinline__ double trsv_fwd(double b, unsigned F, double ldiag, double rdiag) {
-        const bool inF = lane < D && in_mask(F, lane);
-        double s = inF ? b : 0.0;
-        if (kUnroll) {
-#pragma unroll
-            for (int j = 0; j < D; ++j)
-                if (in_mask(F, j)) trsv_fwd_step(j, inF, s);
-        } else {
-#pragma unroll 1
-            for (unsigned mj = F; mj; mj &= mj - 1) trsv_fwd_step(low_bit(mj), inF, s);
-        }
-        return s;
-    }
-    // dense.hpp:229-235 backward solve L^T b = rhs on F, exact order: for i
-    // descending, s = b_i - sum_{j > i ascending} L(j,i) b_j.  Every lane
-    // computes every b_i (redundantly, identical bits).
     __device__ __forceinline__ double trsv_bwd(double b, unsigned F) {
-        double out = b;
-        if (kUnroll) {
-            double bv[D];
-#pragma unroll
-            for (int i = D - 1; i >= 0; --i) {
-                bv[i] = 0.0;
-                if (!in_mask(F, i)) continue;
-                double s = bcast(b, i);
-#pragma unroll
-                for (int j = i + 1; j < D; ++j)
-                    if (in_mask(F, j)) s -= Lw[j + i * D] * bv[j];
-                bv[i] = div_rcp(s, Lw[i + i * D], RD[i]);
-                if (lane == i) out = bv[i];
-            }
-        } else {
-            double* bb = s2 + tog;  // dedicated staging for this solve
-            tog ^= D;
-#pragma unroll 1
-            for (unsigned mi = F; mi; mi &= ~(1u << high_bit(mi))) {
-                const int i = high_bit(mi);
-                double s = bcast(b, i);
-#pragma unroll 1
-                for (unsigned mj = F & ~((2u << i) - 1u); mj; mj &= mj - 1) {
-                    const int j = low_bit(mj);
-                    s -= Lw[j + i * D] * bb[j];
-                }
-                const double bi = div_rcp(s, Lw[i + i * D], RD[i]);
-                if (lane == i) {
-                    out = bi;
-                    bb[i] = bi;
-                }
-                __syncwarp();
-            }
-        }
-        return out;
+        double* bb = s2 + tog;  // staging for the non-unrolled variant
+        tog ^= D;
+        return trsv_bwd_fn<D, kUnroll>(Lw, RD, bb, b, F, lane);
     }
 
     // ------------------------------------------------ tron.hpp:290-344
@@ -575,49 +602,53 @@ struct Warp {
         count(nn);
         double bmin, bmax;
         breakpt(x, mg, l, u, m, bmin, bmax);
-        s = gpstep(x, -alpha, g, l, u, m);
-        bool interpolate;
-        if (nrm2(s, m) > radius) {
-            interpolate = true;
-        } else {
-            double gs;
-            const double q = quad_model(g, s, m, gs);
-            if (!isfinite(q)) return TB_STATUS_EVALUATION_ERROR;
-            count(2 * nn + 1);
-            interpolate = q >= cfg->mu0 * gs;
-        }
-        if (interpolate) {
-            bool search = true;
+        // The reference's initial test, interpolation loop and extrapolation
+        // loop (tron.hpp:210-248) as one state machine with a single trial
+        // site (code size): same trials in the same order, same flops.
+        int mode = 0;  // 0 initial test, 1 interpolate, 2 extrapolate
+        double alpha_good = alpha;
 #pragma unroll 1
-            while (search && alpha > 1e-30) {
-                alpha *= cfg->interp_factor;
-                s = gpstep(x, -alpha, g, l, u, m);
-                if (nrm2(s, m) <= radius) {
-                    double gs;
-                    const double q = quad_model(g, s, m, gs);
-                    if (!isfinite(q)) return TB_STATUS_EVALUATION_ERROR;
-                    count(2 * nn + 1);
-                    search = q >= cfg->mu0 * gs;
-                }
+        for (;;) {
+            s = gpstep(x, -alpha, g, l, u, m);
+            const double nr = nrm2(s, m);
+            // :212 evaluates q unless nrm > radius; :224/:235 only if nrm <= radius
+            const bool evalq = mode == 0 ? !(nr > radius) : (nr <= radius);
+            bool qge = false;  // q >= mu0 g's (q and g's are finite here)
+            if (evalq) {
+                double gs;
+                const double q = quad_model(g, s, m, gs);
+                if (!isfinite(q)) return TB_STATUS_EVALUATION_ERROR;
+                count(2 * nn + 1);
+                qge = q >= cfg->mu0 * gs;
             }
-        } else {
-            double alpha_good = alpha;
-            bool search = true;
-#pragma unroll 1
-            while (search && alpha <= bmax) {
+            if (mode == 0) {
+                if (!evalq || qge) {  // interpolate
+                    mode = 1;
+                    if (!(alpha > 1e-30)) break;
+                    alpha *= cfg->interp_factor;
+                    continue;
+                }
+                mode = 2;  // extrapolate
+                alpha_good = alpha;
+                if (!(alpha <= bmax)) break;
                 alpha *= extrap_factor;
-                s = gpstep(x, -alpha, g, l, u, m);
-                if (nrm2(s, m) <= radius) {
-                    double gs;
-                    const double q = quad_model(g, s, m, gs);
-                    if (!isfinite(q)) return TB_STATUS_EVALUATION_ERROR;
-                    count(2 * nn + 1);
-                    if (q < cfg->mu0 * gs) alpha_good = alpha;
-                    else search = false;
-                } else {
-                    search = false;
-                }
+                continue;
             }
+            if (mode == 1) {
+                const bool search = evalq ? qge : true;
+                if (!search || !(alpha > 1e-30)) break;
+                alpha *= cfg->interp_factor;
+                continue;
+            }
+            if (evalq && !qge) {
+                alpha_good = alpha;
+                if (!(alpha <= bmax)) break;
+                alpha *= extrap_factor;
+                continue;
+            }
+            break;
+        }
+        if (mode == 2) {
             alpha = alpha_good;
             s = gpstep(x, -alpha, g, l, u, m);
         }
