@@ -286,6 +286,7 @@ tbdev::KernelArgs make_args(const tb_problem_batch* b, int64_t np, const tb_tron
     a.prm = np > 0 ? prm : nullptr;
     a.cfg = *cfg;
     a.fast_forward = ff;
+    a.extrap = 1.0 / cfg->interp_factor;
     a.x_star = o.x_star;
     a.f_star = o.f_star;
     a.pg_norm = o.pg;

@@ -102,6 +102,7 @@ struct KernelArgs {
     const double* prm;
     tb_tron_config cfg;
     int fast_forward;
+    double extrap;  // 1.0 / cfg.interp_factor, computed on the host (IEEE, same bits)
     double* x_star;
     double* f_star;
     double* pg_norm;
@@ -529,19 +530,18 @@ struct Warp {
             q = trsv_fwd(q, F, ldiag, rdiag);
             count(2 * nf2);
             const double ptq = dot(p, q, F);
+            // both branches of tron.hpp:315-327 call trqsol(w, p, delta) on
+            // the same inputs: one call site (code size), same result / error
+            double sigma;
+            const int rc = trqsol(w, p, delta, F, sigma);
+            if (rc) return rc;
             if (ptq <= 0.0) {
-                double sigma;
-                const int rc = trqsol(w, p, delta, F, sigma);
-                if (rc) return rc;
                 w += sigma * p;
                 count(2 * nf);
                 cg_status = 2;
                 break;
             }
             const double alpha = rho / ptq;
-            double sigma;
-            const int rc = trqsol(w, p, delta, F, sigma);
-            if (rc) return rc;
             count(1);
             if (alpha >= sigma) {
                 w += sigma * p;
@@ -870,7 +870,7 @@ __global__ void __launch_bounds__(32, TB_MIN_BLOCKS) tron_solve_kernel(const __g
     const long long tb_ph_total0 = clock64();
 #endif
     W.cfg = &a.cfg;
-    W.extrap = 1.0 / a.cfg.interp_factor;
+    W.extrap = a.extrap;
     const int n = a.n;
     const int lane = W.lane;
     const bool act = lane < n;
@@ -899,59 +899,27 @@ __global__ void __launch_bounds__(32, TB_MIN_BLOCKS) tron_solve_kernel(const __g
         status = TB_STATUS_INVALID_BOUNDS;
     } else {
         const double kEta1 = 0.25, kEta2 = 0.75;
+        // tron.hpp:473-549 restructured around ONE family-evaluation site and
+        // ONE gradient site (code size: the branch context is large): pass 0
+        // evaluates the start point (:473-483), pass k >= 1 the trial point of
+        // iteration k (:506-539).  Same operations in the same order.
         x = W.clip(x, l, u);
-        fam.prepare(W, x);
-        f = fam.f(W);
-        W.count(tb_family_flops(FAM, n, 0));
-        f_evals = 1;
-        double g = fam.grad(W);
-        W.count(tb_family_flops(FAM, n, 1));
-        pg = W.pgnorm(x, g, l, u);
-        double delta = cfg.has_delta0 ? cfg.delta0 : tb_smax(W.nrm2(g, W.act), 1.0);
-        double alpha_c = 1.0;
+        double xe = x;  // point being evaluated
+        double g = 0.0, s = 0.0, delta = 0.0, alpha_c = 1.0;
         bool need_hessian = true;
-        status = pg <= cfg.tol_pg ? TB_STATUS_CONVERGED : TB_STATUS_ITER_LIMIT;
-
-        if (status != TB_STATUS_CONVERGED) {
+        long long fl_iter0 = 0, cg_its = 0;
+        double delta_in = 0.0, alpha_in = 0.0;
 #pragma unroll 1
-            for (int iter = 1; iter <= cfg.max_iter; ++iter) {
-                iterations = iter;
-                if (need_hessian) {  // family context holds the current x
-                    TB_PH_BEGIN(0)
-                    fam.hess(W);
-                    TB_PH_END(W, 0)
-                    W.count(tb_family_flops(FAM, n, 2));
-                    need_hessian = false;
-                }
-                const long long fl_iter0 = W.fl;
-                const double delta_in = delta, alpha_in = alpha_c;
-
-                double cs, alpha_new;
-                TB_PH_BEGIN(1)
-                int rc = W.cauchy(x, g, l, u, delta, alpha_c, alpha_new, cs);
-                TB_PH_END(W, 1)
-                if (rc) {
-                    status = rc;
-                    break;
-                }
-                alpha_c = alpha_new;
-                double xt, s;
-                long long cg_its;
-                TB_PH_BEGIN(5)
-                rc = W.subspace_step(x, g, l, u, delta, cs, xt, s, cg_its);
-                TB_PH_END(W, 5)
-                if (rc) {
-                    status = rc;  // FactorizationFailed caught like tron.hpp:499-501
-                    break;
-                }
-                cg_iterations += cg_its;
-                TB_PH_BEGIN(6)
-                fam.prepare(W, xt);
-                const double f_trial = fam.f(W);
-                W.count(tb_family_flops(FAM, n, 0));
-                ++f_evals;
-
-                TB_PH_END(W, 6)
+        for (int iter = 0;; ++iter) {
+            TB_PH_BEGIN(6)
+            fam.prepare(W, xe);
+            const double fe = fam.f(W);
+            W.count(tb_family_flops(FAM, n, 0));
+            ++f_evals;
+            TB_PH_END(W, 6)
+            bool take = iter == 0;  // evaluate the gradient at xe
+            if (iter > 0) {
+                const double f_trial = fe;
                 const double as = W.gemv(s, W.act);
                 double gs, sas, snn;
                 W.seq_sum3(g * s, s * as, s * s, W.act, gs, sas, snn);
@@ -976,19 +944,28 @@ __global__ void __launch_bounds__(32, TB_MIN_BLOCKS) tron_solve_kernel(const __g
                     delta = tb_smax(delta, tb_smin(alphax * snorm, cfg.sigma3 * delta));
                 delta = tb_smin(delta, cfg.delta_max);
                 W.count(12);
-
-                const bool accepted = actred > cfg.eta0 * prered;
-                if (accepted) {
-                    x = xt;
+                take = actred > cfg.eta0 * prered;  // accepted (:529)
+                if (take) {
+                    x = xe;
                     f = f_trial;
-                    g = fam.grad(W);  // context was prepared at xt
-                    W.count(tb_family_flops(FAM, n, 1));
                     need_hessian = true;
-                    pg = W.pgnorm(x, g, l, u);
-                    if (pg <= cfg.tol_pg) {
-                        status = TB_STATUS_CONVERGED;
-                        break;
-                    }
+                }
+            } else {
+                f = fe;
+            }
+            if (take) {
+                g = fam.grad(W);  // the context was prepared at xe
+                W.count(tb_family_flops(FAM, n, 1));
+                pg = W.pgnorm(x, g, l, u);
+            }
+            if (iter == 0) {
+                delta = cfg.has_delta0 ? cfg.delta0 : tb_smax(W.nrm2(g, W.act), 1.0);
+                status = pg <= cfg.tol_pg ? TB_STATUS_CONVERGED : TB_STATUS_ITER_LIMIT;
+                if (status == TB_STATUS_CONVERGED) break;
+            } else {
+                if (take && pg <= cfg.tol_pg) {
+                    status = TB_STATUS_CONVERGED;
+                    break;
                 }
                 if (delta <= 1e-300) break;
                 // Zero-change fixed point: a rejected
@@ -996,7 +973,7 @@ __global__ void __launch_bounds__(32, TB_MIN_BLOCKS) tron_solve_kernel(const __g
                 // unchanged leaves the whole solver state (x, f, g, A, delta,
                 // alpha_c) unchanged, so every remaining iteration replays it
                 // exactly.  Fast-forward with identical counters.
-                if (a.fast_forward && !accepted && iter >= 2 && delta == delta_in && alpha_c == alpha_in) {
+                if (a.fast_forward && !take && iter >= 2 && delta == delta_in && alpha_c == alpha_in) {
                     const long long rem = cfg.max_iter - iter;
                     cg_iterations += rem * cg_its;
                     f_evals += rem;
@@ -1005,6 +982,36 @@ __global__ void __launch_bounds__(32, TB_MIN_BLOCKS) tron_solve_kernel(const __g
                     break;
                 }
             }
+            if (iter + 1 > cfg.max_iter) break;
+            iterations = iter + 1;
+            if (need_hessian) {  // family context holds the current x
+                TB_PH_BEGIN(0)
+                fam.hess(W);
+                TB_PH_END(W, 0)
+                W.count(tb_family_flops(FAM, n, 2));
+                need_hessian = false;
+            }
+            fl_iter0 = W.fl;
+            delta_in = delta;
+            alpha_in = alpha_c;
+
+            double cs, alpha_new;
+            TB_PH_BEGIN(1)
+            int rc = W.cauchy(x, g, l, u, delta, alpha_c, alpha_new, cs);
+            TB_PH_END(W, 1)
+            if (rc) {
+                status = rc;
+                break;
+            }
+            alpha_c = alpha_new;
+            TB_PH_BEGIN(5)
+            rc = W.subspace_step(x, g, l, u, delta, cs, xe, s, cg_its);
+            TB_PH_END(W, 5)
+            if (rc) {
+                status = rc;  // FactorizationFailed caught like tron.hpp:499-501
+                break;
+            }
+            cg_iterations += cg_its;
         }
     }
 
