@@ -134,21 +134,37 @@ int orc_chol_right(int n, const double* A, double shift, double* L) {
 
 /* dense.hpp:182-201 shifted_factorize: alpha = 0, then max(2 alpha, alpha0)
  * up to cap = 1e8 * max(1, max_abs(A)) */
+/* diagnostics: histogram of attempts per shifted_factorize call */
+static long g_ccf_hist[64];
+void orc_debug_ccf_hist(long* out, int clear) {
+    for (int k = 0; k < 64; ++k) {
+        out[k] = __atomic_load_n(&g_ccf_hist[k], __ATOMIC_RELAXED);
+        if (clear) __atomic_store_n(&g_ccf_hist[k], 0, __ATOMIC_RELAXED);
+    }
+}
+static void ccf_hist_add(int attempts) {
+    __atomic_fetch_add(&g_ccf_hist[attempts < 63 ? attempts : 63], 1, __ATOMIC_RELAXED);
+}
+
 static int orc_shifted_factorize(int n, const double* A, double* L, double* shift, int left) {
     double max_diag = 0.0;
     for (int i = 0; i < n; ++i) max_diag = SMAX(max_diag, fabs(A[i + (long)i * n]));
     const double alpha0 = SMAX(1e-3 * max_diag, 1e-8);
     const double cap = 1e8 * SMAX(1.0, orc_max_abs(n, A));
     double alpha = 0.0;
-    for (;;) {
+    for (int att = 1;; ++att) {
         const int ok = left ? orc_chol_left(n, A, alpha, L) : orc_chol_right(n, A, alpha, L);
         if (ok) {
             *shift = alpha;
+            ccf_hist_add(att);
             return 0;
         }
         alpha = SMAX(2.0 * alpha, alpha0);
         g_fl += 1;
-        if (!(alpha <= cap)) return TB_STATUS_FACTORIZATION_FAILED;
+        if (!(alpha <= cap)) {
+            ccf_hist_add(0);
+            return TB_STATUS_FACTORIZATION_FAILED;
+        }
     }
 }
 
