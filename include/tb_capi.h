@@ -152,6 +152,58 @@ int64_t tb_kernel_launch_count(void);
  * the TRON kernel; measured, not nominal). */
 int tb_measure_fp64_peak(int32_t device, double* tflops);
 
+
+/* ---- ADMM AC-OPF (the reference ships no code for it) ---
+ * Device-resident component ADMM whose branch stage is the batched TRON
+ * kernel.  One process per GPU: branches are sharded in equal chunks; after
+ * tb_admm_solve_components the caller all-gathers the branch solutions (NCCL)
+ * into the buffer of tb_admm_branch_solution, then tb_admm_update_consensus
+ * runs the bus / multiplier / residual step and leaves this shard's residual
+ * maxima for a max-allreduce.  Single process: tb_admm_step. */
+typedef struct tb_admm_grid {
+    int32_t n_bus, n_gen, n_branch;
+    const double *bus_pd, *bus_qd, *bus_gsh, *bus_bsh, *bus_vmin, *bus_vmax; /* [n_bus], per unit */
+    const int32_t* gen_bus;                                                  /* [n_gen] */
+    const double *gen_c2, *gen_c1, *gen_pmin, *gen_pmax, *gen_qmin, *gen_qmax;
+    const int32_t *br_from, *br_to; /* [n_branch] */
+    const double* br_coef;          /* [n_branch][8] pi-model flow coefficients (TB_BR_GFF..TB_BR_BTF) */
+} tb_admm_grid;
+
+typedef struct tb_admm_options {
+    double rho_pq; /* power couplings (rho0 = 10) */
+    double rho_va; /* voltage / angle couplings (4 rho0) */
+    int32_t shard_rank, shard_count;
+    tb_tron_config tron;
+} tb_admm_options;
+
+typedef struct tb_admm tb_admm;
+
+#define TB_ADMM_GEN_P 0
+#define TB_ADMM_GEN_Q 1
+#define TB_ADMM_GEN_PT 2
+#define TB_ADMM_GEN_QT 3
+#define TB_ADMM_GEN_LP 4
+#define TB_ADMM_GEN_LQ 5
+#define TB_ADMM_BUS_WT 6
+#define TB_ADMM_BUS_TT 7
+#define TB_ADMM_BRANCH_X 8      /* [n_branch][4] (v_i, v_j, th_i, th_j) */
+#define TB_ADMM_BRANCH_PARAMS 9 /* [n_branch][36] incl. lambda / rho / consensus */
+#define TB_ADMM_BRANCH_STATUS 10
+#define TB_ADMM_COST 11 /* sum_g c2 p^2 + c1 p */
+
+void tb_admm_options_default(tb_admm_options* opt);
+/* x_external: optional device buffer for the branch solutions,
+ * ceil(n_branch / shard_count) * shard_count rows of 4 doubles (NULL: owned) */
+int tb_admm_create(const tb_admm_grid* grid, const tb_admm_options* opt, int32_t device, double* x_external,
+                   tb_admm** out);
+int tb_admm_destroy(tb_admm* a);
+int tb_admm_solve_components(tb_admm* a, void* stream);
+int tb_admm_branch_solution(tb_admm* a, double** x_dev, int64_t* lo, int64_t* hi);
+int tb_admm_update_consensus(tb_admm* a, void* stream, double* res2_dev);
+int tb_admm_step(tb_admm* a, double* primal, double* dual);
+int tb_admm_get(tb_admm* a, int32_t what, void* host_out);
+const char* tb_admm_last_error(void);
+
 #ifdef __cplusplus
 }
 #endif

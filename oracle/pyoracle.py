@@ -166,3 +166,62 @@ def run_unit_tests(which="oracle"):
     exe = ORACLE_TESTS if which == "oracle" else REF_TESTS
     p = subprocess.run([exe], capture_output=True, text=True)
     return p.returncode, p.stdout
+
+
+class OracleAdmm:
+    """CPU ADMM oracle (oracle/admm_oracle.c): same closed forms as the
+    device (csrc/tb_admm.h), branch stage through the C TRON restatement."""
+
+    def __init__(self, grid, options=None, workers=1):
+        from paper_2106_14995_b200.admm import AdmmOptions
+
+        self.lib = oracle_lib().lib
+        self.grid = grid
+        g, self._keep = grid.to_c()
+        o = (options or AdmmOptions()).to_c(0, 1)
+        h = C.c_void_p()
+        self.lib.orc_admm_create.argtypes = [C.c_void_p, C.c_void_p, C.c_int, C.POINTER(C.c_void_p)]
+        assert self.lib.orc_admm_create(C.addressof(g), C.addressof(o), int(workers), C.byref(h)) == 0
+        self._g, self._o = g, o
+        self._h = h
+        self.history = []
+
+    def step(self):
+        p, d = C.c_double(), C.c_double()
+        self.lib.orc_admm_step.argtypes = [C.c_void_p, C.POINTER(C.c_double), C.POINTER(C.c_double)]
+        rc = self.lib.orc_admm_step(self._h, C.byref(p), C.byref(d))
+        assert rc == 0, f"TRON error status {rc} in the branch stage"
+        self.history.append((p.value, d.value))
+        return p.value, d.value
+
+    def get(self, what):
+        from paper_2106_14995_b200 import admm as A
+
+        g = self.grid
+        shapes = {A.BRANCH_X: ((g.n_branch, 4), np.float64), A.BRANCH_PARAMS: ((g.n_branch, 36), np.float64),
+                  A.BRANCH_STATUS: ((g.n_branch,), np.int32), A.BUS_WT: ((g.n_bus,), np.float64),
+                  A.BUS_TT: ((g.n_bus,), np.float64), A.COST: ((1,), np.float64)}
+        shape, dt = shapes.get(what, ((g.n_gen,), np.float64))
+        out = np.zeros(shape, dt)
+        self.lib.orc_admm_get.argtypes = [C.c_void_p, C.c_int, C.c_void_p]
+        assert self.lib.orc_admm_get(self._h, int(what), out.ctypes.data) == 0
+        return out
+
+    def close(self):
+        if self._h:
+            self.lib.orc_admm_destroy.argtypes = [C.c_void_p]
+            self.lib.orc_admm_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def admm_gen_p(c2, c1, lam, rho, ptil, pmin, pmax):
+    f = oracle_lib().lib.orc_admm_gen_p
+    f.restype = C.c_double
+    f.argtypes = [C.c_double] * 7
+    return f(c2, c1, lam, rho, ptil, pmin, pmax)

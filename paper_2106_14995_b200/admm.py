@@ -1,0 +1,224 @@
+"""Device-resident component ADMM for AC-OPF over the C ABI
+(tb_admm_*), with the batched TRON kernel as its branch stage.
+
+Single GPU:      AdmmSolver(grid).run(iters)
+One process per GPU (torchrun): ShardedAdmm(grid, rank, world, device) —
+branches sharded in equal chunks; per iteration one NCCL all-gather of the
+branch solutions (the consensus exchange: exact, no arithmetic) and one
+max-allreduce of the two residuals.  Every process then holds bit-identical
+state, equal to the single-GPU run and to the CPU oracle.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+from typing import List, Optional, Tuple
+
+import numpy as np
+
+from . import _lib as L
+from .tron import SolverError, TronConfig
+
+GEN_P, GEN_Q, GEN_PT, GEN_QT, GEN_LP, GEN_LQ, BUS_WT, BUS_TT = range(8)
+BRANCH_X, BRANCH_PARAMS, BRANCH_STATUS, COST = 8, 9, 10, 11
+
+
+@dataclass
+class Grid:
+    """Network in per unit (SPEC.md:325 NetworkCase minus parsing)."""
+
+    bus_pd: np.ndarray
+    bus_qd: np.ndarray
+    bus_gsh: np.ndarray
+    bus_bsh: np.ndarray
+    bus_vmin: np.ndarray
+    bus_vmax: np.ndarray
+    gen_bus: np.ndarray
+    gen_c2: np.ndarray
+    gen_c1: np.ndarray
+    gen_pmin: np.ndarray
+    gen_pmax: np.ndarray
+    gen_qmin: np.ndarray
+    gen_qmax: np.ndarray
+    br_from: np.ndarray
+    br_to: np.ndarray
+    br_coef: np.ndarray  # [n_branch, 8]
+
+    @property
+    def n_bus(self):
+        return len(self.bus_pd)
+
+    @property
+    def n_gen(self):
+        return len(self.gen_bus)
+
+    @property
+    def n_branch(self):
+        return len(self.br_from)
+
+    def to_c(self):
+        """tb_admm_grid pointing at contiguous copies (kept alive by the return)."""
+        keep = {}
+        g = GridC()
+        g.n_bus, g.n_gen, g.n_branch = self.n_bus, self.n_gen, self.n_branch
+        for name, _ in GridC._fields_[3:]:
+            a = getattr(self, name)
+            a = np.ascontiguousarray(a, dtype=np.int32 if name in ("gen_bus", "br_from", "br_to") else np.float64)
+            keep[name] = a
+            setattr(g, name, a.ctypes.data)
+        return g, keep
+
+
+class GridC(C.Structure):
+    _fields_ = [("n_bus", C.c_int32), ("n_gen", C.c_int32), ("n_branch", C.c_int32)] + [
+        (n, C.c_void_p) for n in ("bus_pd", "bus_qd", "bus_gsh", "bus_bsh", "bus_vmin", "bus_vmax", "gen_bus",
+                                  "gen_c2", "gen_c1", "gen_pmin", "gen_pmax", "gen_qmin", "gen_qmax", "br_from",
+                                  "br_to", "br_coef")]
+
+
+class OptionsC(C.Structure):
+    _fields_ = [("rho_pq", C.c_double), ("rho_va", C.c_double), ("shard_rank", C.c_int32),
+                ("shard_count", C.c_int32), ("tron", L.TronConfigC)]
+
+
+@dataclass
+class AdmmOptions:
+    rho_pq: float = 10.0  # SPEC.md:426 rho0
+    rho_va: float = 40.0  # 4 rho0
+    tron: TronConfig = field(default_factory=TronConfig)
+
+    def to_c(self, rank=0, world=1) -> OptionsC:
+        o = OptionsC()
+        o.rho_pq, o.rho_va, o.shard_rank, o.shard_count = self.rho_pq, self.rho_va, rank, world
+        o.tron = self.tron.to_c()
+        return o
+
+
+_SIG = {
+    "tb_admm_create": (C.c_int, [C.POINTER(GridC), C.POINTER(OptionsC), C.c_int32, C.c_void_p, C.POINTER(C.c_void_p)]),
+    "tb_admm_destroy": (C.c_int, [C.c_void_p]),
+    "tb_admm_solve_components": (C.c_int, [C.c_void_p, C.c_void_p]),
+    "tb_admm_branch_solution": (C.c_int, [C.c_void_p, C.POINTER(C.c_void_p), C.POINTER(C.c_int64), C.POINTER(C.c_int64)]),
+    "tb_admm_update_consensus": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p]),
+    "tb_admm_step": (C.c_int, [C.c_void_p, C.POINTER(C.c_double), C.POINTER(C.c_double)]),
+    "tb_admm_get": (C.c_int, [C.c_void_p, C.c_int32, C.c_void_p]),
+    "tb_admm_last_error": (C.c_char_p, []),
+    "tb_admm_options_default": (None, [C.POINTER(OptionsC)]),
+}
+
+
+def _lib():
+    lib = L.load()
+    for n, (res, args) in _SIG.items():
+        fn = getattr(lib, n)
+        fn.restype, fn.argtypes = res, args
+    return lib
+
+
+class AdmmSolver:
+    """One GPU (or one shard of a multi-process run)."""
+
+    def __init__(self, grid: Grid, options: AdmmOptions = None, device: int = 0, rank: int = 0, world: int = 1,
+                 x_buffer_ptr: Optional[int] = None):
+        self.lib = _lib()
+        self.grid = grid
+        self.options = options or AdmmOptions()
+        g, self._keep = grid.to_c()
+        o = self.options.to_c(rank, world)
+        h = C.c_void_p()
+        if self.lib.tb_admm_create(C.byref(g), C.byref(o), device, C.c_void_p(x_buffer_ptr or 0), C.byref(h)) != 0:
+            raise SolverError(self.lib.tb_admm_last_error().decode())
+        self._h = h
+        self.history: List[Tuple[float, float]] = []
+
+    def close(self):
+        if getattr(self, "_h", None):
+            self.lib.tb_admm_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def _check(self, rc):
+        if rc != 0:
+            raise SolverError(self.lib.tb_admm_last_error().decode())
+
+    def step(self) -> Tuple[float, float]:
+        """One ADMM iteration (single process): returns (primal, dual)."""
+        p, d = C.c_double(), C.c_double()
+        self._check(self.lib.tb_admm_step(self._h, C.byref(p), C.byref(d)))
+        self.history.append((p.value, d.value))
+        return p.value, d.value
+
+    def run(self, max_iter: int, tol_primal: float = 0.0, tol_dual: float = 0.0):
+        """admm_solve until both residuals <= tol or max_iter."""
+        for _ in range(max_iter):
+            p, d = self.step()
+            if p <= tol_primal and d <= tol_dual:
+                break
+        return self.history
+
+    # phases for the multi-process path
+    def solve_components(self, stream: int = 0):
+        self._check(self.lib.tb_admm_solve_components(self._h, C.c_void_p(stream or 0)))
+
+    def branch_solution(self):
+        x, lo, hi = C.c_void_p(), C.c_int64(), C.c_int64()
+        self._check(self.lib.tb_admm_branch_solution(self._h, C.byref(x), C.byref(lo), C.byref(hi)))
+        return x.value, lo.value, hi.value
+
+    def update_consensus(self, stream: int = 0, res2_dev_ptr: int = 0):
+        self._check(self.lib.tb_admm_update_consensus(self._h, C.c_void_p(stream or 0), C.c_void_p(res2_dev_ptr)))
+
+    def get(self, what: int) -> np.ndarray:
+        g = self.grid
+        if what == COST:
+            out = np.zeros(1)
+        elif what in (BRANCH_X,):
+            out = np.zeros((g.n_branch, 4))
+        elif what == BRANCH_PARAMS:
+            out = np.zeros((g.n_branch, 36))
+        elif what == BRANCH_STATUS:
+            out = np.zeros(g.n_branch, np.int32)
+        elif what in (BUS_WT, BUS_TT):
+            out = np.zeros(g.n_bus)
+        else:
+            out = np.zeros(g.n_gen)
+        self._check(self.lib.tb_admm_get(self._h, what, out.ctypes.data))
+        return out
+
+
+class ShardedAdmm:
+    """One process per GPU under torch.distributed (NCCL): the C5 path."""
+
+    def __init__(self, grid: Grid, rank: int, world: int, device: int, options: AdmmOptions = None):
+        import torch
+
+        self.torch = torch
+        self.dev = torch.device("cuda", device)
+        chunk = (grid.n_branch + world - 1) // world
+        self.chunk, self.rank, self.world = chunk, rank, world
+        # the branch-solution buffer the all-gather writes into (caller-owned)
+        self.x = torch.zeros((chunk * world, 4), dtype=torch.float64, device=self.dev)
+        self.res = torch.zeros(2, dtype=torch.float64, device=self.dev)
+        self.solver = AdmmSolver(grid, options, device, rank, world, x_buffer_ptr=self.x.data_ptr())
+        self.history: List[Tuple[float, float]] = []
+
+    def step(self) -> Tuple[float, float]:
+        import torch.distributed as dist
+
+        st = self.torch.cuda.current_stream(self.dev).cuda_stream
+        st = st if st != 0 else 1  # cudaStreamLegacy
+        self.solver.solve_components(st)
+        if self.world > 1:  # consensus exchange: in-place all-gather of the branch solutions
+            mine = self.x[self.rank * self.chunk:(self.rank + 1) * self.chunk]
+            dist.all_gather_into_tensor(self.x, mine)
+        self.solver.update_consensus(st, self.res.data_ptr())
+        if self.world > 1:
+            dist.all_reduce(self.res, op=dist.ReduceOp.MAX)
+        p, d = self.res.tolist()
+        self.history.append((p, d))
+        return p, d

@@ -1,0 +1,347 @@
+// admm.cu — device-resident component ADMM for AC-OPF,
+// driving the batched TRON kernel for the branch subproblems.
+//
+// Per iteration, all on the device of this process:
+//   admm_gen_kernel        generator closed form (all generators)
+//   tron_solve_kernel      branch subproblems of this shard (warm start, in place)
+//   [exchange]             the caller all-gathers the branch solutions x
+//                          (NCCL over NVLink when sharded; nothing when not)
+//   admm_bus_kernel        bus consensus + multipliers + residual terms (every
+//                          bus, deterministic; residual max over this shard's
+//                          buses -> the caller max-allreduces two doubles)
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/tb_capi.h"
+#include "tb_admm.h"
+#include "tb_admm_host.h"
+#include "tron_device.cuh"
+#include "tron_launch.h"
+
+namespace {
+
+__global__ void admm_gen_kernel(tb_admm_view v) {
+    const int g = blockIdx.x * blockDim.x + threadIdx.x;
+    if (g < v.n_gen) tb_admm_gen_update(&v, g);
+}
+
+// residuals are non-negative doubles: unsigned max on the bit patterns
+__device__ __forceinline__ void atomic_max_nonneg(unsigned long long* a, double x) {
+    atomicMax(a, (unsigned long long)__double_as_longlong(x));
+}
+
+__global__ void admm_bus_kernel(tb_admm_view v, int res_lo, int res_hi, unsigned long long* res) {
+    const int b = blockIdx.x * blockDim.x + threadIdx.x;
+    tb_admm_res r = {0.0, 0.0};
+    if (b < v.n_bus) {
+        tb_admm_bus_update(&v, b, &r);
+        if (b < res_lo || b >= res_hi) r.primal = r.dual = 0.0;
+        if (!(r.primal >= 0.0)) r.primal = CUDART_INF;  // NaN -> report as inf
+        if (!(r.dual >= 0.0)) r.dual = CUDART_INF;
+    }
+    const double p = tbdev::warp_max_nonneg(r.primal);
+    const double d = tbdev::warp_max_nonneg(r.dual);
+    if ((threadIdx.x & 31) == 0) {
+        atomic_max_nonneg(res + 0, p);
+        atomic_max_nonneg(res + 1, d);
+    }
+}
+
+__global__ void admm_cost_kernel(tb_admm_view v, double* out) {
+    // deterministic order: one thread sums all generators ascending
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        double s = 0.0;
+        for (int g = 0; g < v.n_gen; ++g) s += tb_admm_gen_cost(&v, g);
+        *out = s;
+    }
+}
+
+thread_local std::string g_admm_err;
+
+int fail(int code, const std::string& m) {
+    g_admm_err = m;
+    return code;
+}
+
+}  // namespace
+
+struct tb_admm {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    tb_context* ctx = nullptr;
+    tb_admm_view v{};           // device pointers
+    std::vector<void*> allocs;  // owned device buffers
+    double* x = nullptr;        // [n_rows][4] branch solutions (owned or caller's)
+    double *lower = nullptr, *upper = nullptr;
+    int32_t* status = nullptr;
+    unsigned long long* res = nullptr;
+    double* cost = nullptr;
+    int64_t br_lo = 0, br_hi = 0;
+    int bus_lo = 0, bus_hi = 0;
+    tb_tron_config tron{};
+    long long iterations = 0;
+};
+
+namespace {
+
+template <typename T>
+T* dalloc(tb_admm* a, size_t n, cudaError_t* err) {
+    void* p = nullptr;
+    cudaError_t e = cudaMalloc(&p, sizeof(T) * (n ? n : 1));
+    if (e != cudaSuccess) *err = e;
+    else a->allocs.push_back(p);
+    return static_cast<T*>(p);
+}
+
+template <typename T>
+cudaError_t upload(T* dst, const T* src, size_t n) {
+    return n ? cudaMemcpy(dst, src, sizeof(T) * n, cudaMemcpyHostToDevice) : cudaSuccess;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* tb_admm_last_error(void) { return g_admm_err.c_str(); }
+
+void tb_admm_options_default(tb_admm_options* o) {
+    std::memset(o, 0, sizeof(*o));
+    o->rho_pq = 10.0;
+    o->rho_va = 40.0;  // 4 * rho0
+    o->shard_rank = 0;
+    o->shard_count = 1;
+    tb_config_default(&o->tron);
+}
+
+int tb_admm_create(const tb_admm_grid* gr, const tb_admm_options* opt, int32_t device, double* x_external,
+                   tb_admm** out) {
+    if (!gr || !opt || !out) return fail(TB_E_INVALID_ARGUMENT, "tb_admm_create: null argument");
+    *out = nullptr;
+    if (gr->n_bus < 1 || gr->n_branch < 1 || gr->n_gen < 0)
+        return fail(TB_E_INVALID_ARGUMENT, "tb_admm_create: empty network");
+    if (opt->shard_count < 1 || opt->shard_rank < 0 || opt->shard_rank >= opt->shard_count)
+        return fail(TB_E_INVALID_ARGUMENT, "tb_admm_create: bad shard");
+    if (!(opt->rho_pq > 0.0) || !(opt->rho_va > 0.0)) return fail(TB_E_INVALID_ARGUMENT, "tb_admm_create: rho must be > 0");
+    if (tb_config_validate(&opt->tron) != TB_OK) return fail(TB_E_INVALID_ARGUMENT, tb_last_error());
+    const int nb = gr->n_bus, ng = gr->n_gen, nl = gr->n_branch;
+    for (int l = 0; l < nl; ++l)
+        if (gr->br_from[l] < 0 || gr->br_from[l] >= nb || gr->br_to[l] < 0 || gr->br_to[l] >= nb)
+            return fail(TB_E_INVALID_ARGUMENT, "tb_admm_create: branch endpoint out of range");
+    for (int g = 0; g < ng; ++g)
+        if (gr->gen_bus[g] < 0 || gr->gen_bus[g] >= nb)
+            return fail(TB_E_INVALID_ARGUMENT, "tb_admm_create: generator bus out of range");
+
+    // host-side initial state (shared init rules, tb_admm_host.h semantics)
+    tb_admm_host_state hs;
+    if (tb_admm_host_init(gr, opt, &hs) != 0) return fail(TB_E_INVALID_ARGUMENT, hs.err);
+    for (int b = 0; b < nb; ++b)
+        if (hs.end_ptr[b + 1] == hs.end_ptr[b]) {
+            tb_admm_host_free(&hs);
+            return fail(TB_E_INVALID_ARGUMENT, "tb_admm_create: bus " + std::to_string(b) + " has no branch");
+        }
+
+    tb_admm* a = new tb_admm;
+    a->device = device;
+    a->tron = opt->tron;
+    int prev = 0;
+    cudaGetDevice(&prev);
+    cudaError_t err = cudaSetDevice(device);
+    if (err == cudaSuccess) err = cudaStreamCreateWithFlags(&a->stream, cudaStreamNonBlocking);
+    const int64_t chunk = (nl + opt->shard_count - 1) / opt->shard_count;  // padded chunks for all-gather
+    const int64_t rows = chunk * opt->shard_count;
+    a->br_lo = std::min<int64_t>(nl, chunk * opt->shard_rank);
+    a->br_hi = std::min<int64_t>(nl, chunk * (opt->shard_rank + 1));
+    {
+        const int base = nb / opt->shard_count, rem = nb % opt->shard_count;
+        int lo = 0;
+        for (int k = 0; k < opt->shard_rank; ++k) lo += base + (k < rem ? 1 : 0);
+        a->bus_lo = lo;
+        a->bus_hi = lo + base + (opt->shard_rank < rem ? 1 : 0);
+    }
+    tb_admm_view& v = a->v;
+    v.n_bus = nb;
+    v.n_gen = ng;
+    v.n_branch = nl;
+    v.branch_dim = 4;
+#define ALLOC_UP(field, T, n, src)                                       \
+    do {                                                                 \
+        T* p_ = dalloc<T>(a, (n), &err);                                 \
+        if (err == cudaSuccess) err = upload<T>(p_, (src), (n));         \
+        v.field = p_;                                                    \
+    } while (0)
+    if (err == cudaSuccess) {
+        ALLOC_UP(bus_pd, double, nb, gr->bus_pd);
+        ALLOC_UP(bus_qd, double, nb, gr->bus_qd);
+        ALLOC_UP(bus_gsh, double, nb, gr->bus_gsh);
+        ALLOC_UP(bus_bsh, double, nb, gr->bus_bsh);
+        ALLOC_UP(bus_wt, double, nb, hs.bus_wt);
+        ALLOC_UP(bus_tt, double, nb, hs.bus_tt);
+        ALLOC_UP(gen_bus, int32_t, ng, gr->gen_bus);
+        ALLOC_UP(gen_c2, double, ng, gr->gen_c2);
+        ALLOC_UP(gen_c1, double, ng, gr->gen_c1);
+        ALLOC_UP(gen_pmin, double, ng, gr->gen_pmin);
+        ALLOC_UP(gen_pmax, double, ng, gr->gen_pmax);
+        ALLOC_UP(gen_qmin, double, ng, gr->gen_qmin);
+        ALLOC_UP(gen_qmax, double, ng, gr->gen_qmax);
+        ALLOC_UP(gen_p, double, ng, hs.gen_p);
+        ALLOC_UP(gen_q, double, ng, hs.gen_q);
+        ALLOC_UP(gen_lp, double, ng, hs.gen_lp);
+        ALLOC_UP(gen_lq, double, ng, hs.gen_lq);
+        ALLOC_UP(gen_rp, double, ng, hs.gen_rp);
+        ALLOC_UP(gen_rq, double, ng, hs.gen_rq);
+        ALLOC_UP(gen_pt, double, ng, hs.gen_pt);
+        ALLOC_UP(gen_qt, double, ng, hs.gen_qt);
+        ALLOC_UP(br_from, int32_t, nl, gr->br_from);
+        ALLOC_UP(br_to, int32_t, nl, gr->br_to);
+        ALLOC_UP(br_params, double, (size_t)nl * TB_BR_NPARAMS, hs.br_params);
+        ALLOC_UP(gen_ptr, int32_t, nb + 1, hs.gen_ptr);
+        ALLOC_UP(gen_idx, int32_t, ng, hs.gen_idx);
+        ALLOC_UP(end_ptr, int32_t, nb + 1, hs.end_ptr);
+        ALLOC_UP(end_idx, int32_t, 2 * nl, hs.end_idx);
+    }
+#undef ALLOC_UP
+    if (err == cudaSuccess) {
+        if (x_external) a->x = x_external;
+        else a->x = dalloc<double>(a, (size_t)rows * 4, &err);
+    }
+    if (err == cudaSuccess) err = upload<double>(a->x, hs.br_x, (size_t)nl * 4);
+    if (err == cudaSuccess) {
+        a->lower = dalloc<double>(a, (size_t)nl * 4, &err);
+        if (err == cudaSuccess) err = upload<double>(a->lower, hs.br_lower, (size_t)nl * 4);
+        a->upper = dalloc<double>(a, (size_t)nl * 4, &err);
+        if (err == cudaSuccess) err = upload<double>(a->upper, hs.br_upper, (size_t)nl * 4);
+        a->status = dalloc<int32_t>(a, (size_t)nl, &err);
+        a->res = dalloc<unsigned long long>(a, 2, &err);
+        a->cost = dalloc<double>(a, 1, &err);
+    }
+    v.br_x = a->x;
+    tb_admm_host_free(&hs);
+    if (err == cudaSuccess) {
+        const int32_t dev = device;
+        if (tb_context_create(&dev, 1, &a->ctx) != TB_OK) err = cudaErrorUnknown;
+    }
+    cudaSetDevice(prev);
+    if (err != cudaSuccess) {
+        std::string m = std::string("tb_admm_create: ") + cudaGetErrorString(err);
+        tb_admm_destroy(a);
+        return fail(TB_E_CUDA, m);
+    }
+    *out = a;
+    return TB_OK;
+}
+
+int tb_admm_destroy(tb_admm* a) {
+    if (!a) return TB_OK;
+    int prev = 0;
+    cudaGetDevice(&prev);
+    cudaSetDevice(a->device);
+    if (a->stream) cudaStreamSynchronize(a->stream);
+    for (void* p : a->allocs) cudaFree(p);
+    if (a->stream) cudaStreamDestroy(a->stream);
+    if (a->ctx) tb_context_destroy(a->ctx);
+    cudaSetDevice(prev);
+    delete a;
+    return TB_OK;
+}
+
+// generator update (all generators) + branch TRON on this shard, enqueued on
+// `stream` (NULL: the ADMM's own stream); returns without synchronising.
+int tb_admm_solve_components(tb_admm* a, void* stream) {
+    if (!a) return fail(TB_E_INVALID_ARGUMENT, "null admm");
+    cudaSetDevice(a->device);
+    cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : a->stream;
+    if (a->v.n_gen > 0) admm_gen_kernel<<<(a->v.n_gen + 127) / 128, 128, 0, st>>>(a->v);
+    const int64_t cnt = a->br_hi - a->br_lo;
+    if (cnt > 0) {
+        tb_problem_batch b{TB_FAMILY_BRANCH, 4, cnt, a->x + a->br_lo * 4, a->lower + a->br_lo * 4,
+                           a->upper + a->br_lo * 4, a->v.br_params + a->br_lo * TB_BR_NPARAMS, TB_BR_NPARAMS,
+                           TB_MEM_DEVICE};
+        tb_batch_result r{};
+        r.x_star = a->x + a->br_lo * 4;  // in place: each warp reads its x0 before writing x*
+        r.status = a->status + a->br_lo;
+        r.memspace = TB_MEM_DEVICE;
+        const int rc = tb_solve_batch_async(a->ctx, &b, &a->tron, &r, st);
+        if (rc != TB_OK) return fail(rc, tb_last_error());
+    }
+    const cudaError_t e = cudaGetLastError();
+    return e == cudaSuccess ? TB_OK : fail(TB_E_CUDA, cudaGetErrorString(e));
+}
+
+// device branch-solution buffer [rows][4]; this shard owns rows [lo, hi);
+// rows are padded to shard_count equal chunks of `chunk` rows for all-gather
+int tb_admm_branch_solution(tb_admm* a, double** x_dev, int64_t* lo, int64_t* hi) {
+    if (!a) return fail(TB_E_INVALID_ARGUMENT, "null admm");
+    *x_dev = a->x;
+    *lo = a->br_lo;
+    *hi = a->br_hi;
+    return TB_OK;
+}
+
+// bus consensus + multipliers over every bus (needs the complete x), residual
+// maxima over this shard's buses written to res2_dev[0..1] (device doubles) if
+// non-NULL; enqueued on `stream`.
+int tb_admm_update_consensus(tb_admm* a, void* stream, double* res2_dev) {
+    if (!a) return fail(TB_E_INVALID_ARGUMENT, "null admm");
+    cudaSetDevice(a->device);
+    cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : a->stream;
+    cudaMemsetAsync(a->res, 0, 2 * sizeof(unsigned long long), st);
+    admm_bus_kernel<<<(a->v.n_bus + 127) / 128, 128, 0, st>>>(a->v, a->bus_lo, a->bus_hi, a->res);
+    if (res2_dev) cudaMemcpyAsync(res2_dev, a->res, 2 * sizeof(double), cudaMemcpyDeviceToDevice, st);
+    ++a->iterations;
+    const cudaError_t e = cudaGetLastError();
+    return e == cudaSuccess ? TB_OK : fail(TB_E_CUDA, cudaGetErrorString(e));
+}
+
+// one full iteration in a single process (no exchange needed), blocking;
+// primal / dual residuals to host
+int tb_admm_step(tb_admm* a, double* primal, double* dual) {
+    int rc = tb_admm_solve_components(a, nullptr);
+    if (rc) return rc;
+    rc = tb_admm_update_consensus(a, nullptr, nullptr);
+    if (rc) return rc;
+    double r[2];
+    cudaError_t e = cudaMemcpyAsync(r, a->res, sizeof r, cudaMemcpyDeviceToHost, a->stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(a->stream);
+    if (e != cudaSuccess) return fail(TB_E_CUDA, cudaGetErrorString(e));
+    if (primal) *primal = r[0];
+    if (dual) *dual = r[1];
+    return TB_OK;
+}
+
+// copy a state array to host: what = TB_ADMM_*
+int tb_admm_get(tb_admm* a, int32_t what, void* host_out) {
+    if (!a || !host_out) return fail(TB_E_INVALID_ARGUMENT, "null argument");
+    cudaSetDevice(a->device);
+    cudaStreamSynchronize(a->stream);
+    const tb_admm_view& v = a->v;
+    const void* src = nullptr;
+    size_t bytes = 0;
+    switch (what) {
+        case TB_ADMM_GEN_P: src = v.gen_p; bytes = sizeof(double) * v.n_gen; break;
+        case TB_ADMM_GEN_Q: src = v.gen_q; bytes = sizeof(double) * v.n_gen; break;
+        case TB_ADMM_GEN_PT: src = v.gen_pt; bytes = sizeof(double) * v.n_gen; break;
+        case TB_ADMM_GEN_QT: src = v.gen_qt; bytes = sizeof(double) * v.n_gen; break;
+        case TB_ADMM_GEN_LP: src = v.gen_lp; bytes = sizeof(double) * v.n_gen; break;
+        case TB_ADMM_GEN_LQ: src = v.gen_lq; bytes = sizeof(double) * v.n_gen; break;
+        case TB_ADMM_BUS_WT: src = v.bus_wt; bytes = sizeof(double) * v.n_bus; break;
+        case TB_ADMM_BUS_TT: src = v.bus_tt; bytes = sizeof(double) * v.n_bus; break;
+        case TB_ADMM_BRANCH_X: src = a->x; bytes = sizeof(double) * 4 * (size_t)v.n_branch; break;
+        case TB_ADMM_BRANCH_PARAMS: src = v.br_params; bytes = sizeof(double) * TB_BR_NPARAMS * (size_t)v.n_branch; break;
+        case TB_ADMM_BRANCH_STATUS: src = a->status; bytes = sizeof(int32_t) * (size_t)v.n_branch; break;
+        case TB_ADMM_COST: {
+            admm_cost_kernel<<<1, 1, 0, a->stream>>>(a->v, a->cost);
+            src = a->cost;
+            bytes = sizeof(double);
+            break;
+        }
+        default: return fail(TB_E_INVALID_ARGUMENT, "tb_admm_get: unknown field");
+    }
+    const cudaError_t e = cudaMemcpy(host_out, src, bytes, cudaMemcpyDeviceToHost);
+    return e == cudaSuccess ? TB_OK : fail(TB_E_CUDA, cudaGetErrorString(e));
+}
+
+}  // extern "C"

@@ -176,3 +176,57 @@ def make(family: str, count: int, dim: int, seed: int = None) -> ProblemBatch:
     if family in ("branch", "branch4", "branch6"):
         return branch(count, dim, seed if seed is not None else 2)
     raise ValueError(family)
+
+
+# ------------------------------------------------------------------ ADMM grids
+def grid(n_bus: int, n_branch: int, n_gen: int, seed: int = 4, load_factor: float = 0.6, shunt_frac: float = 0.1):
+    """Synthetic AC-OPF network: random spanning tree plus
+    extra edges up to n_branch, pi-model branches like C2, generators on
+    random buses, loads at `load_factor` of generation capacity.  Returns an
+    admm.Grid (per-unit)."""
+    from .admm import Grid
+
+    assert n_branch >= n_bus - 1 and n_bus >= 2
+    rng = Stream(seed, 1, salt=900 + n_bus)
+    u = lambda k, lo=0.0, hi=1.0: rng.uniform(k, lo, hi)[0]  # noqa: E731
+    parent = np.floor(u(n_bus - 1) * np.arange(1, n_bus)).astype(np.int64)  # parent < child
+    frm = [parent]
+    to = [np.arange(1, n_bus)]
+    extra = n_branch - (n_bus - 1)
+    if extra > 0:
+        a = np.floor(u(extra) * n_bus).astype(np.int64)
+        b = np.floor(u(extra) * (n_bus - 1)).astype(np.int64)
+        b = np.where(b >= a, b + 1, b)  # b != a
+        frm.append(a)
+        to.append(b)
+    br_from = np.concatenate(frm).astype(np.int32)
+    br_to = np.concatenate(to).astype(np.int32)
+    r = u(n_branch, 0.001, 0.05)
+    x = u(n_branch, 0.01, 0.3)
+    bc = u(n_branch, 0.0, 0.1)
+    tap = np.where(u(n_branch) < 0.2, u(n_branch, 0.95, 1.05), 1.0)
+    coef = pi_model(r, x, bc, tap)
+    gen_bus = np.sort(np.floor(u(n_gen) * n_bus).astype(np.int32))
+    pmax = u(n_gen, 0.5, 5.0)
+    w = u(n_bus, 0.0, 1.0)
+    pd = load_factor * pmax.sum() * w / w.sum()
+    qd = pd * u(n_bus, 0.1, 0.4)
+    sh = u(n_bus) < shunt_frac
+    return Grid(
+        bus_pd=pd, bus_qd=qd, bus_gsh=np.where(sh, u(n_bus, 0.0, 0.01), 0.0),
+        bus_bsh=np.where(sh, u(n_bus, 0.0, 0.1), 0.0), bus_vmin=np.full(n_bus, 0.9), bus_vmax=np.full(n_bus, 1.1),
+        gen_bus=gen_bus, gen_c2=u(n_gen, 0.005, 0.05), gen_c1=u(n_gen, 1.0, 10.0), gen_pmin=np.zeros(n_gen),
+        gen_pmax=pmax, gen_qmin=-0.5 * pmax, gen_qmax=0.5 * pmax, br_from=br_from, br_to=br_to,
+        br_coef=np.ascontiguousarray(coef))
+
+
+def two_bus(pd: float = 0.5, qd: float = 0.1, r: float = 0.01, x: float = 0.1):
+    """SPEC.md:411 single-branch 2-bus toy: one generator at bus 0, one load at bus 1."""
+    from .admm import Grid
+
+    coef = pi_model(np.array([r]), np.array([x]), np.array([0.0]), np.array([1.0]))
+    return Grid(bus_pd=np.array([0.0, pd]), bus_qd=np.array([0.0, qd]), bus_gsh=np.zeros(2), bus_bsh=np.zeros(2),
+                bus_vmin=np.full(2, 0.9), bus_vmax=np.full(2, 1.1), gen_bus=np.array([0], np.int32),
+                gen_c2=np.array([0.1]), gen_c1=np.array([1.0]), gen_pmin=np.array([0.0]), gen_pmax=np.array([2.0]),
+                gen_qmin=np.array([-1.0]), gen_qmax=np.array([1.0]), br_from=np.array([0], np.int32),
+                br_to=np.array([1], np.int32), br_coef=np.ascontiguousarray(coef))
