@@ -163,6 +163,67 @@ def run_reference_arm(args, rank, world):
     return 0
 
 
+def run_admm(args, rank, world, local, dev):
+    """ADMM iterations/s: C4 (13,659 buses / 20,467 branches / 4,092 gens) on
+    one GPU; C5 (70,000 branches, ~46.7k buses) sharded over N GPUs with an
+    NCCL all-gather of the branch solutions + max-allreduce of the residuals
+    per iteration.  Each timed iteration = generator + branch TRON + exchange +
+    bus/multiplier/residual kernels + the residual read-back."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2106_14995_b200 import admm as A
+    from paper_2106_14995_b200 import synth
+
+    if world == 1:
+        cfg, grid = "C4", synth.grid(13659, 20467, 4092)
+    else:
+        nb = int(round(70000 * 13659 / 20467))
+        cfg, grid = "C5", synth.grid(nb, 70000, int(0.3 * nb))
+    if world > 1 and not dist.is_initialized():
+        return None
+    run = A.ShardedAdmm(grid, rank, world, local)
+    for _ in range(max(3, args.warmup)):
+        run.step()
+    stream = torch.cuda.current_stream(dev)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize(dev)
+    e0.record(stream)
+    for _ in range(args.admm_iters):
+        run.step()
+    e1.record(stream)
+    torch.cuda.synchronize(dev)
+    ms = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(ms, op=dist.ReduceOp.MAX)
+    ms_iter = float(ms.item()) / args.admm_iters
+    line = {"metric": "ADMM iterations/sec", "value": 1e3 / ms_iter, "unit": "iter/s", "ms_per_iter": ms_iter,
+            "iters_timed": args.admm_iters, "warmup_iters": max(3, args.warmup),
+            "config": {"workload": cfg, "n_bus": grid.n_bus, "n_branch": grid.n_branch, "n_gen": grid.n_gen,
+                       "branch_dim": 4, "parallelism": f"branches sharded over {world} GPU(s), NCCL all-gather"},
+            "residuals_first_last": [run.history[0], run.history[-1]]}
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            from oracle import pyoracle
+
+            cores = os.cpu_count() or 1
+            cpu = pyoracle.OracleAdmm(grid, workers=cores)
+            cpu.step()
+            t0 = time.perf_counter()
+            k = 3
+            for _ in range(k):
+                cpu.step()
+            v = k / (time.perf_counter() - t0)
+            line["cpu_baseline"] = {"value": v, "unit": "iter/s", "cores": cores, "kind": "port",
+                                    "sample": f"iterations 2-4 of the same {cfg} ADMM run, oracle/admm_oracle.c "
+                                              f"(branch stage through the C TRON restatement, {cores} threads)"}
+        except Exception as e:
+            line["cpu_baseline"] = {"value": None, "sample": f"failed: {e}"}
+    return line
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -171,6 +232,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--batch", type=int, default=BATCH)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-admm", action="store_true")
+    ap.add_argument("--admm-iters", type=int, default=20)
     args = ap.parse_args()
     args.warmup = max(3, args.warmup) if args.impl == "ours" else args.warmup
 
@@ -314,6 +377,10 @@ def main():
         except Exception as e:
             cpu = {"value": None, "unit": "solves/s", "cores": None, "kind": "reference", "sample": f"failed: {e}"}
 
+    admm_line = None
+    if not args.no_admm:
+        admm_line = run_admm(args, rank, world, local, dev)
+
     traffic = None
     prof = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(prof):
@@ -342,6 +409,7 @@ def main():
             "gpu_launches": int(launches),
             "parity": parity,
             "status_counts": {str(k): int(v) for k, v in zip(*np.unique(status, return_counts=True))},
+            "admm": admm_line,
             "ms_per_step_all": ms_steps,
         }
         print(json.dumps(line), flush=True)

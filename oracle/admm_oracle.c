@@ -166,3 +166,31 @@ double orc_admm_gen_p(double c2, double c1, double lam, double rho, double ptil,
     tb_admm_gen_update(&v, 0);
     return p;
 }
+
+/* ---- phases (the sharded scheme of paper_2106_14995_b200/admm.py, on CPU) */
+/* generator update (all) + branch TRON for rows [lo, hi) in place */
+int orc_admm_solve_components(orc_admm* a, int64_t lo, int64_t hi) {
+    for (int g = 0; g < a->ng; ++g) tb_admm_gen_update(&a->v, g);
+    if (hi <= lo) return 0;
+    const int64_t cnt = hi - lo;
+    const int rc = orc_solve_batch(TB_FAMILY_BRANCH, 4, cnt, a->hs.br_x + lo * 4, a->hs.br_lower + lo * 4,
+                                   a->hs.br_upper + lo * 4, a->hs.br_params + lo * TB_BR_NPARAMS, TB_BR_NPARAMS,
+                                   &a->opt.tron, a->workers, a->xtmp, NULL, NULL, a->status + lo, NULL, NULL, NULL,
+                                   NULL, NULL, NULL, NULL);
+    memcpy(a->hs.br_x + lo * 4, a->xtmp, sizeof(double) * 4 * (size_t)cnt);
+    return rc;
+}
+double* orc_admm_x(orc_admm* a) { return a->hs.br_x; }
+/* bus update over every bus; residual maxima over buses [blo, bhi) */
+void orc_admm_update_consensus(orc_admm* a, int blo, int bhi, double* primal, double* dual) {
+    double pr = 0.0, du = 0.0;
+    for (int b = 0; b < a->nb; ++b) {
+        tb_admm_res r;
+        tb_admm_bus_update(&a->v, b, &r);
+        if (b < blo || b >= bhi) continue;
+        if (pr < r.primal) pr = r.primal;
+        if (du < r.dual) du = r.dual;
+    }
+    *primal = pr;
+    *dual = du;
+}

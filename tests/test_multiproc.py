@@ -65,3 +65,70 @@ def test_gloo_world2_sharded_equals_single_process():
     ref = po.solve_batch(synth.branch(1001, 6, seed=2), impl="oracle")
     for k, v in got.items():
         assert np.array_equal(v, getattr(ref, k)), k
+
+
+def _admm_worker(rank, world, port, q):
+    """One rank of the sharded ADMM scheme (paper_2106_14995_b200/admm.py
+    ShardedAdmm) with the CPU oracle as the compute backend and gloo as the
+    collective: equal branch chunks, in-place all-gather of the branch
+    solutions, bus update on every rank, max-allreduce of the residuals."""
+    import ctypes as C
+    import sys
+
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    import torch
+    import torch.distributed as dist
+
+    from oracle import pyoracle as po
+    from paper_2106_14995_b200 import synth
+    from paper_2106_14995_b200.shard import partition
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    g = synth.grid(150, 210, 40, seed=9, shunt_frac=0.3)
+    a = po.OracleAdmm(g)
+    lib = a.lib
+    lib.orc_admm_solve_components.argtypes = [C.c_void_p, C.c_int64, C.c_int64]
+    lib.orc_admm_x.argtypes = [C.c_void_p]
+    lib.orc_admm_x.restype = C.POINTER(C.c_double)
+    lib.orc_admm_update_consensus.argtypes = [C.c_void_p, C.c_int, C.c_int, C.POINTER(C.c_double),
+                                              C.POINTER(C.c_double)]
+    chunk = (g.n_branch + world - 1) // world
+    lo, hi = min(g.n_branch, rank * chunk), min(g.n_branch, (rank + 1) * chunk)
+    blo, bhi = partition(g.n_bus, world)[rank]
+    xs = np.ctypeslib.as_array(lib.orc_admm_x(a._h), shape=(g.n_branch * 4,))
+    buf = torch.zeros(chunk * world * 4, dtype=torch.float64)
+    hist = []
+    for _ in range(12):
+        assert lib.orc_admm_solve_components(a._h, lo, hi) == 0
+        buf[: g.n_branch * 4] = torch.from_numpy(xs)
+        dist.all_gather_into_tensor(buf, buf[rank * chunk * 4:(rank + 1) * chunk * 4].clone())
+        xs[:] = buf[: g.n_branch * 4].numpy()
+        p, d = C.c_double(), C.c_double()
+        lib.orc_admm_update_consensus(a._h, blo, bhi, C.byref(p), C.byref(d))
+        r = torch.tensor([p.value, d.value], dtype=torch.float64)
+        dist.all_reduce(r, op=dist.ReduceOp.MAX)
+        hist.append(tuple(r.tolist()))
+    if rank == 0:
+        q.put(hist)
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_gloo_world2_sharded_admm_equals_single_process():
+    from oracle import pyoracle as po
+    from paper_2106_14995_b200 import synth
+
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_admm_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    hist = q.get(timeout=180)
+    for p in procs:
+        p.join(timeout=180)
+        assert p.exitcode == 0
+    a = po.OracleAdmm(synth.grid(150, 210, 40, seed=9, shunt_frac=0.3))
+    ref = [a.step() for _ in range(12)]
+    assert hist == ref
