@@ -24,7 +24,10 @@ def test_library_exports_every_declared_symbol():
     assert len(names) >= 12
     for n in names:
         assert hasattr(lib, n), n
-    assert set(names) == set(_lib.SIGNATURES), "ctypes signatures must cover the header exactly"
+    from paper_2106_14995_b200 import admm
+
+    bound = set(_lib.SIGNATURES) | set(admm._SIG)
+    assert set(names) == bound, f"ctypes signatures must cover the header exactly: {set(names) ^ bound}"
 
 
 def test_config_defaults_match_reference():
