@@ -68,6 +68,7 @@ struct DevState {
     DevBuf in;   // x0, lower, upper, params
     DevBuf out;  // results
     DevBuf flag;
+    DevBuf ws;   // block-kernel workspace (d > 32)
 };
 
 __global__ void first_error_kernel(const int32_t* status, long long count, unsigned long long* out) {
@@ -170,6 +171,7 @@ int tb_context_destroy(tb_context* ctx) {
         d.in.release();
         d.out.release();
         d.flag.release();
+        d.ws.release();
     }
     cudaSetDevice(prev);
     delete ctx;
@@ -220,9 +222,9 @@ int check_batch(const tb_problem_batch* b, int64_t* nparams) {
         return set_err(TB_E_INVALID_ARGUMENT, "solve_batch: unknown problem family %d", b->family);
     if (!tb_family_dim_ok(b->family, b->dim))
         return set_err(TB_E_INVALID_ARGUMENT, "solve_batch: dimension %d invalid for family %d", b->dim, b->family);
-    if (b->dim > tbdev::max_warp_dim())
+    if (b->dim > tbdev::max_dim())
         return set_err(TB_E_INVALID_ARGUMENT, "solve_batch: dimension %d exceeds device capacity %d", b->dim,
-                       tbdev::max_warp_dim());
+                       tbdev::max_dim());
     *nparams = tb_fam_nparams(b->family, b->dim);
     if (b->count > 0) {
         if (!b->x0 || !b->lower || !b->upper)
@@ -296,7 +298,20 @@ tbdev::KernelArgs make_args(const tb_problem_batch* b, int64_t np, const tb_tron
     a.f_evals = o.fev;
     a.wall_time = o.wall;
     a.flops = o.flops;
+    a.ws = nullptr;
+    a.ws_bytes = 0;
     return a;
+}
+
+// attach the block kernel's workspace (d > 32), grown on demand
+cudaError_t attach_ws(DevState& d, int family, tbdev::KernelArgs& a) {
+    size_t need = 0;
+    cudaError_t e = tbdev::tron_ws_need(family, a.n, a.count, &need);
+    if (e != cudaSuccess || need == 0) return e;
+    if ((e = d.ws.ensure(need)) != cudaSuccess) return e;
+    a.ws = d.ws.p;
+    a.ws_bytes = d.ws.cap;
+    return cudaSuccess;
 }
 
 }  // namespace
@@ -317,6 +332,7 @@ extern "C" int tb_solve_batch_async(tb_context* ctx, const tb_problem_batch* b, 
               r->wall_time};
     tbdev::KernelArgs a = make_args(b, np, cfg, ctx->fast_forward, b->x0, b->lower, b->upper, b->params,
                                     b->params_stride, b->count, o);
+    CUDA_TRY(attach_ws(d, b->family, a));
     CUDA_TRY(tbdev::launch_tron(b->family, a, st));
     if (b->count > 0) ++g_launches;
     return TB_OK;
@@ -389,6 +405,7 @@ extern "C" int tb_solve_batch(tb_context* ctx, const tb_problem_batch* b, const 
             }
         }
         tbdev::KernelArgs a = make_args(b, np, cfg, ctx->fast_forward, x0, lw, up, prm, stride, c, o);
+        CUDA_TRY(attach_ws(d, b->family, a));
         CUDA_TRY(cudaEventRecord(d.ev[1], d.stream));
         CUDA_TRY(tbdev::launch_tron(b->family, a, d.stream));
         if (c > 0) ++g_launches;

@@ -112,6 +112,10 @@ struct KernelArgs {
     int64_t* f_evals;
     double* wall_time;
     int64_t* flops;
+    // block kernel (d > 32) only: global workspace (work counter + per-block
+    // Hessian slices) and its size in bytes
+    void* ws;
+    size_t ws_bytes;
 };
 
 // shared memory per warp (doubles; every region starts at an even offset)

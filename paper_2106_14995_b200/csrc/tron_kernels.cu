@@ -9,6 +9,9 @@ cudaError_t launch_hs45(const KernelArgs& a, cudaStream_t st);
 cudaError_t launch_boxqp(const KernelArgs& a, cudaStream_t st);
 cudaError_t launch_ncvx(const KernelArgs& a, cudaStream_t st);
 cudaError_t launch_branch(const KernelArgs& a, cudaStream_t st);
+cudaError_t ws_need_hs45(int n, long long count, size_t* bytes);
+cudaError_t ws_need_boxqp(int n, long long count, size_t* bytes);
+cudaError_t ws_need_ncvx(int n, long long count, size_t* bytes);
 
 cudaError_t launch_tron(int family, const KernelArgs& a, cudaStream_t st) {
     if (a.count <= 0) return cudaSuccess;
@@ -21,5 +24,18 @@ cudaError_t launch_tron(int family, const KernelArgs& a, cudaStream_t st) {
     return cudaErrorInvalidValue;
 }
 
+// workspace bytes launch_tron needs in KernelArgs::ws (0 for the warp kernel)
+cudaError_t tron_ws_need(int family, int n, long long count, size_t* bytes) {
+    *bytes = 0;
+    if (count <= 0) return cudaSuccess;
+    switch (family) {
+        case TB_FAMILY_HS45: return ws_need_hs45(n, count, bytes);
+        case TB_FAMILY_BOXQP: return ws_need_boxqp(n, count, bytes);
+        case TB_FAMILY_NCVX: return ws_need_ncvx(n, count, bytes);
+    }
+    return cudaSuccess;
+}
+
 int max_warp_dim() { return 32; }
+int max_dim() { return 128; }
 }  // namespace tbdev

@@ -3,6 +3,9 @@
 #pragma once
 #include <cuda_runtime.h>
 
+#include <cstdlib>
+
+#include "tron_block.cuh"
 #include "tron_device.cuh"
 
 namespace tbdev {
@@ -23,6 +26,69 @@ static cudaError_t launch_fdc(const KernelArgs& a, cudaStream_t st) {
 template <int FAM, int D>
 static cudaError_t launch_fd(const KernelArgs& a, cudaStream_t st) {
     return a.flops ? launch_fdc<FAM, D, true>(a, st) : launch_fdc<FAM, D, false>(a, st);
+}
+
+// ---------------------------------------------------------------- d > 32
+// Hessian placement of the block kernel: TB_BLOCK_ASMEM=1 keeps A in shared
+// memory (fewer resident problems per SM), default 0 keeps it in the
+// L2-resident global workspace.
+inline bool blk_asmem() {
+    const char* e = std::getenv("TB_BLOCK_ASMEM");
+    return e && e[0] == '1';
+}
+
+// persistent grid: resident blocks per SM x SMs, capped by the batch
+template <int FAM, int D, bool ASMEM, bool COUNT>
+static cudaError_t blk_grid(long long count, long long* grid, size_t* smem_out) {
+    using SL = BlkLayout<D, ASMEM>;
+    const size_t smem = sizeof(double) * (size_t)SL::total();
+    auto kern = tron_block_kernel<FAM, D, ASMEM, COUNT>;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    int dev = 0, sms = 0, per_sm = 0;
+    if ((e = cudaGetDevice(&dev)) != cudaSuccess) return e;
+    if ((e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev)) != cudaSuccess) return e;
+    if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, D, smem)) != cudaSuccess) return e;
+    if (per_sm < 1) return cudaErrorInvalidConfiguration;
+    *grid = count < (long long)sms * per_sm ? count : (long long)sms * per_sm;
+    *smem_out = smem;
+    return cudaSuccess;
+}
+
+template <int FAM, int D, bool ASMEM, bool COUNT>
+static cudaError_t launch_blk_c(const KernelArgs& a, cudaStream_t st) {
+    long long grid = 0;
+    size_t smem = 0;
+    cudaError_t e = blk_grid<FAM, D, ASMEM, COUNT>(a.count, &grid, &smem);
+    if (e != cudaSuccess) return e;
+    const size_t need = kBlkWsHeader + (ASMEM ? 0 : sizeof(double) * (size_t)grid * D * D);
+    if (!a.ws || a.ws_bytes < need) return cudaErrorMemoryAllocation;
+    if ((e = cudaMemsetAsync(a.ws, 0, sizeof(unsigned), st)) != cudaSuccess) return e;
+    tron_block_kernel<FAM, D, ASMEM, COUNT><<<(unsigned)grid, D, smem, st>>>(a);
+    return cudaGetLastError();
+}
+
+template <int FAM, int D>
+static cudaError_t launch_blk(const KernelArgs& a, cudaStream_t st) {
+    if (blk_asmem())
+        return a.flops ? launch_blk_c<FAM, D, true, true>(a, st) : launch_blk_c<FAM, D, true, false>(a, st);
+    return a.flops ? launch_blk_c<FAM, D, false, true>(a, st) : launch_blk_c<FAM, D, false, false>(a, st);
+}
+
+// workspace bytes the block kernel needs for `count` problems of dim n
+template <int FAM, int D>
+static cudaError_t ws_need_blk(long long count, size_t* bytes) {
+    long long grid = 0;
+    size_t smem = 0;
+    *bytes = kBlkWsHeader;
+    if (blk_asmem()) return cudaSuccess;
+    cudaError_t e = blk_grid<FAM, D, false, false>(count, &grid, &smem);
+    if (e != cudaSuccess) return e;
+    long long g2 = 0;
+    if ((e = blk_grid<FAM, D, false, true>(count, &g2, &smem)) != cudaSuccess) return e;
+    if (g2 > grid) grid = g2;
+    *bytes += sizeof(double) * (size_t)grid * D * D;
+    return cudaSuccess;
 }
 
 }  // namespace tbdev

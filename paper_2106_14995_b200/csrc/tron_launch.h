@@ -9,4 +9,6 @@ struct KernelArgs;
 namespace tbdev {
 cudaError_t launch_tron(int family, const KernelArgs& a, cudaStream_t st);
 int max_warp_dim();
+int max_dim();
+cudaError_t tron_ws_need(int family, int n, long long count, size_t* bytes);
 }  // namespace tbdev

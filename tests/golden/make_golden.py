@@ -29,15 +29,23 @@ CASES = {
     "c3_ncvx_d8": lambda: synth.ncvx(256, 8, seed=11),
     "c3_ncvx_d16": lambda: synth.ncvx(64, 16, seed=19),
     "c3_ncvx_d32": lambda: synth.ncvx(32, 32, seed=35),
+    # d > 32: the block kernel (D = 64 / 128 threads)
+    "c3_ncvx_d64": lambda: synth.ncvx(16, 64, seed=67),
+    "c3_ncvx_d128": lambda: synth.ncvx(8, 128, seed=131),
+    "boxqp_d48": lambda: synth.boxqp(16, 48, seed=53),
     # tests/unit/tron_test.cpp:196-212 shapes
     "boxqp_d4": lambda: synth.boxqp(256, 4, seed=5),
     "hs45_d8": lambda: synth.hs45(4, 8),
+    "hs45_d64": lambda: synth.hs45(2, 64),  # batch.hpp:15 kDefaultCapacity
 }
 
 
 def main():
     assert pyoracle.ref_available(), "build oracle/_ref first: make -C oracle ref"
+    only = set(sys.argv[1:])  # optional: regenerate just these fixtures
     for name, mk in CASES.items():
+        if only and name not in only:
+            continue
         b = mk()
         r = pyoracle.solve_batch(b, impl="ref", workers=os.cpu_count() or 1)
         assert r.rc == 0, (name, pyoracle.last_error())

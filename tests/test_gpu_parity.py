@@ -41,7 +41,7 @@ def test_branch_bitwise(solver, dim):
 
 
 @pytest.mark.parametrize("d", [1, 2, 4, 8, 16, 32])
-def test_hs45(solver, d):
+def test_hs45(solver, d):  # d > 32: test_block_kernel_boxqp_hs45_bitwise
     """SPEC acceptance 1: x*_i = i, f* = 120 - n!"""
     b = synth.hs45(4, d)
     res = solver.solve_batch(b)
@@ -201,9 +201,52 @@ def test_device_memspace_and_stream_async(solver):
     assert_bitwise(out, ref, label="async stream")
 
 
-def test_dimension_over_warp_capacity_rejected(solver):
+def test_dimension_over_device_capacity_rejected(solver):
     with pytest.raises(ValueError):
-        solver.solve_batch(synth.ncvx(2, 33))
+        solver.solve_batch(synth.ncvx(2, 129))
+
+
+# ------------------------------------------------- d > 32: the block kernel
+@pytest.mark.parametrize("asmem", ["0", "1"])
+@pytest.mark.parametrize("d", [33, 40, 64, 65, 100, 128])
+def test_block_kernel_ncvx_bitwise(solver, monkeypatch, d, asmem):
+    """C3 sweep past one warp: D = 64 / 128 threads per problem, Hessian in
+    the global workspace (default) or in shared memory (TB_BLOCK_ASMEM=1);
+    every field, and the flop counters, bit-identical to the oracle."""
+    monkeypatch.setenv("TB_BLOCK_ASMEM", asmem)
+    n = 48 if d <= 64 else 16
+    b = synth.ncvx(n, d, seed=3 + d)
+    res = solver.solve_batch(b, count_flops=True)
+    ref = po.solve_batch(b, impl="oracle", workers=os.cpu_count() or 8)
+    assert_bitwise(res, ref, label=f"ncvx d={d} asmem={asmem}")
+    assert np.array_equal(host(res.flops), ref.flops)
+    assert_bitwise(solver.solve_batch(b), ref, label=f"ncvx d={d} (no count)")
+
+
+@pytest.mark.parametrize("d", [36, 64, 96])
+def test_block_kernel_boxqp_hs45_bitwise(solver, d):
+    for b in (synth.boxqp(24, d, seed=d), synth.hs45(2, min(d, 64))):
+        assert_bitwise(solver.solve_batch(b), po.solve_batch(b, impl="oracle"), label=f"d={d} fam={b.family}")
+
+
+def test_block_kernel_more_problems_than_resident_blocks(solver):
+    """The persistent grid takes problems from a work counter: a batch several
+    times the resident capacity, with config variants and outside starts."""
+    b = synth.ncvx(2000, 40, seed=9)
+    x0 = b.x0 * 3.0
+    cfg = TronConfig(max_iter=7, cg_tol=0.3)
+    res = solver.solve_batch(b, x0, cfg=cfg)
+    assert_bitwise(res, po.solve_batch(b, x0, cfg=cfg, impl="oracle", workers=os.cpu_count() or 8), label="2000x40")
+
+
+def test_block_kernel_device_memspace(solver):
+    import torch
+
+    b = synth.ncvx(64, 70, seed=70)
+    dev = torch.device("cuda", 0)
+    t = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(dev)  # noqa: E731
+    db = ProblemBatch(b.family, 70, t(b.lower), t(b.upper), t(b.params), t(b.x0))
+    assert_bitwise(solver.solve_batch(db), po.solve_batch(b, impl="oracle", workers=8), label="device d=70")
 
 
 def test_hs45_acceptance_all_n(solver):
