@@ -142,6 +142,14 @@ void orc_debug_ccf_hist(long* out, int clear) {
         if (clear) __atomic_store_n(&g_ccf_hist[k], 0, __ATOMIC_RELAXED);
     }
 }
+/* diagnostics: histogram of free-set sizes nf per face pass (bins of 8) */
+static long g_nf_hist[17];
+void orc_debug_nf_hist(long* out, int clear) {
+    for (int k = 0; k < 17; ++k) {
+        out[k] = __atomic_load_n(&g_nf_hist[k], __ATOMIC_RELAXED);
+        if (clear) __atomic_store_n(&g_nf_hist[k], 0, __ATOMIC_RELAXED);
+    }
+}
 static void ccf_hist_add(int attempts) {
     __atomic_fetch_add(&g_ccf_hist[attempts < 63 ? attempts : 63], 1, __ATOMIC_RELAXED);
 }
@@ -474,6 +482,7 @@ static int orc_subspace_step(int n, const double* x0, const double* g, const dou
     double* Lf = (double*)malloc(sizeof(double) * (size_t)m * m);
     for (int faces = 0; faces < n; ++faces) {
         const int nf = orc_select_free_set(n, x_out, l, u, F);
+        __atomic_fetch_add(&g_nf_hist[(nf + 7) / 8 < 16 ? (nf + 7) / 8 : 16], 1, __ATOMIC_RELAXED);
         if (nf == 0) break;
         for (int j = 0; j < nf; ++j)
             for (int i = 0; i < nf; ++i) B[i + (long)j * nf] = A[F[i] + (long)F[j] * n];

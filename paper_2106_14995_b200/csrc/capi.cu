@@ -64,7 +64,9 @@ struct DevBuf {
 struct DevState {
     int device = 0;
     cudaStream_t stream = nullptr;
+    cudaStream_t aux[8] = {};  // one stream per chunk of the host-buffer pipeline
     cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+    cudaEvent_t fork = nullptr, join = nullptr;
     DevBuf in;   // x0, lower, upper, params
     DevBuf out;  // results
     DevBuf flag;
@@ -145,7 +147,10 @@ int tb_context_create(const int32_t* devices, int32_t n_devices, tb_context** ou
         }
         cudaSetDevice(d.device);
         cudaError_t e = cudaStreamCreateWithFlags(&d.stream, cudaStreamNonBlocking);
+        for (int i = 0; i < 8 && e == cudaSuccess; ++i) e = cudaStreamCreateWithFlags(&d.aux[i], cudaStreamNonBlocking);
         for (int i = 0; i < 4 && e == cudaSuccess; ++i) e = cudaEventCreate(&d.ev[i]);
+        if (e == cudaSuccess) e = cudaEventCreateWithFlags(&d.fork, cudaEventDisableTiming);
+        if (e == cudaSuccess) e = cudaEventCreateWithFlags(&d.join, cudaEventDisableTiming);
         if (e != cudaSuccess) {
             delete ctx;
             cudaSetDevice(prev);
@@ -165,9 +170,15 @@ int tb_context_destroy(tb_context* ctx) {
     for (auto& d : ctx->devs) {
         cudaSetDevice(d.device);
         cudaStreamSynchronize(d.stream);
+        for (auto& a : d.aux)
+            if (a) cudaStreamSynchronize(a);
         for (auto& e : d.ev)
             if (e) cudaEventDestroy(e);
+        if (d.fork) cudaEventDestroy(d.fork);
+        if (d.join) cudaEventDestroy(d.join);
         if (d.stream) cudaStreamDestroy(d.stream);
+        for (auto& a : d.aux)
+            if (a) cudaStreamDestroy(a);
         d.in.release();
         d.out.release();
         d.flag.release();
@@ -237,6 +248,9 @@ int check_batch(const tb_problem_batch* b, int64_t* nparams) {
         return set_err(TB_E_INVALID_ARGUMENT, "solve_batch: bad memspace");
     return TB_OK;
 }
+
+constexpr int64_t kChunkMin = 4096;  // problems per chunk of the host-buffer pipeline
+constexpr int64_t kMaxChunks = 8;
 
 struct OutPtrs {
     double *x_star, *f_star, *pg;
@@ -370,60 +384,98 @@ extern "C" int tb_solve_batch(tb_context* ctx, const tb_problem_batch* b, const 
         }
     }
 
+    // Host buffers: the partition is cut into chunks, each on its own stream,
+    // so the H2D copy of chunk i+1 and the D2H copy of chunk i-1 overlap the
+    // solves, and a long-running problem in one chunk never holds back the
+    // next chunk (warp kernel; the persistent block kernel owns one workspace
+    // per device and runs unchunked).
     for (int k = 0; k < G; ++k) {
         DevState& d = ctx->devs[k];
         CUDA_TRY(cudaSetDevice(d.device));
         const int64_t c = cnt[k];
         CUDA_TRY(cudaEventRecord(d.ev[0], d.stream));
-        const double *x0 = b->x0 + lo[k] * n, *lw = b->lower + lo[k] * n, *up = b->upper + lo[k] * n;
-        const double* prm = np > 0 ? b->params + lo[k] * stride : nullptr;
-        if (in_host && c > 0) {
-            const size_t vb = sizeof(double) * (size_t)c * n;
-            const size_t pb = sizeof(double) * (size_t)c * stride;
-            CUDA_TRY(d.in.ensure(3 * vb + pb + 64));
-            char* p = static_cast<char*>(d.in.p);
-            CUDA_TRY(cudaMemcpyAsync(p, x0, vb, cudaMemcpyHostToDevice, d.stream));
-            CUDA_TRY(cudaMemcpyAsync(p + vb, lw, vb, cudaMemcpyHostToDevice, d.stream));
-            CUDA_TRY(cudaMemcpyAsync(p + 2 * vb, up, vb, cudaMemcpyHostToDevice, d.stream));
-            if (pb) CUDA_TRY(cudaMemcpyAsync(p + 3 * vb, prm, pb, cudaMemcpyHostToDevice, d.stream));
-            x0 = reinterpret_cast<const double*>(p);
-            lw = reinterpret_cast<const double*>(p + vb);
-            up = reinterpret_cast<const double*>(p + 2 * vb);
-            prm = pb ? reinterpret_cast<const double*>(p + 3 * vb) : nullptr;
+        const bool staged = (in_host || out_host) && c > 0;
+        const int nch = (staged && n <= tbdev::max_warp_dim() && c >= 2 * kChunkMin)
+                            ? (int)std::min<int64_t>(kMaxChunks, c / kChunkMin)
+                            : 1;
+        if (nch > 1) {
+            CUDA_TRY(cudaEventRecord(d.fork, d.stream));
+            for (int ch = 0; ch < nch; ++ch) CUDA_TRY(cudaStreamWaitEvent(d.aux[ch], d.fork, 0));
         }
-        OutPtrs o;
+        const size_t vb = sizeof(double) * (size_t)c * n;
+        const size_t pb = sizeof(double) * (size_t)c * stride;
+        char* inp = nullptr;
+        if (in_host && c > 0) {
+            CUDA_TRY(d.in.ensure(3 * vb + pb + 64));
+            inp = static_cast<char*>(d.in.p);
+        }
+        OutPtrs ofull;
         if (out_host) {
             CUDA_TRY(d.out.ensure(out_bytes(c, n)));
-            o = carve(d.out.p, c, n);
+            ofull = carve(d.out.p, c, n);
         } else {
-            o = OutPtrs{r->x_star, r->f_star, r->pg_norm, r->status, r->iterations, r->cg_iterations,
-                        r->f_evals, r->flops, r->wall_time};
+            ofull = OutPtrs{r->x_star, r->f_star, r->pg_norm, r->status, r->iterations, r->cg_iterations,
+                            r->f_evals, r->flops, r->wall_time};
             // status is needed for the error scan even if the caller skips it
-            if (!o.status) {
+            if (!ofull.status) {
                 CUDA_TRY(d.out.ensure(out_bytes(c, n)));
-                o.status = carve(d.out.p, c, n).status;
+                ofull.status = carve(d.out.p, c, n).status;
             }
         }
-        tbdev::KernelArgs a = make_args(b, np, cfg, ctx->fast_forward, x0, lw, up, prm, stride, c, o);
-        CUDA_TRY(attach_ws(d, b->family, a));
-        CUDA_TRY(cudaEventRecord(d.ev[1], d.stream));
-        CUDA_TRY(tbdev::launch_tron(b->family, a, d.stream));
-        if (c > 0) ++g_launches;
-        CUDA_TRY(cudaEventRecord(d.ev[2], d.stream));
-        if (out_host && c > 0) {
-            auto cp = [&](void* dst, const void* src, size_t bytes) -> cudaError_t {
-                if (!dst) return cudaSuccess;
-                return cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, d.stream);
-            };
-            CUDA_TRY(cp(r->x_star ? r->x_star + lo[k] * n : nullptr, o.x_star, sizeof(double) * c * n));
-            CUDA_TRY(cp(r->f_star ? r->f_star + lo[k] : nullptr, o.f_star, sizeof(double) * c));
-            CUDA_TRY(cp(r->pg_norm ? r->pg_norm + lo[k] : nullptr, o.pg, sizeof(double) * c));
-            CUDA_TRY(cp(r->status ? r->status + lo[k] : nullptr, o.status, sizeof(int32_t) * c));
-            CUDA_TRY(cp(r->iterations ? r->iterations + lo[k] : nullptr, o.iters, sizeof(int32_t) * c));
-            CUDA_TRY(cp(r->cg_iterations ? r->cg_iterations + lo[k] : nullptr, o.cg, sizeof(int64_t) * c));
-            CUDA_TRY(cp(r->f_evals ? r->f_evals + lo[k] : nullptr, o.fev, sizeof(int64_t) * c));
-            CUDA_TRY(cp(r->flops ? r->flops + lo[k] : nullptr, o.flops, sizeof(int64_t) * c));
-            CUDA_TRY(cp(r->wall_time ? r->wall_time + lo[k] : nullptr, o.wall, sizeof(double) * c));
+        for (int ch = 0; ch < nch; ++ch) {
+            cudaStream_t st = nch > 1 ? d.aux[ch] : d.stream;
+            const int64_t a0 = c * ch / nch, a1 = c * (ch + 1) / nch, cc = a1 - a0;  // local range
+            const int64_t g0 = lo[k] + a0;                                             // global index
+            const double *x0 = b->x0 + g0 * n, *lw = b->lower + g0 * n, *up = b->upper + g0 * n;
+            const double* prm = np > 0 ? b->params + g0 * stride : nullptr;
+            if (in_host && cc > 0) {
+                const size_t cvb = sizeof(double) * (size_t)cc * n, cpb = sizeof(double) * (size_t)cc * stride;
+                char* dx = inp + sizeof(double) * (size_t)a0 * n;
+                char* dl = inp + vb + sizeof(double) * (size_t)a0 * n;
+                char* du = inp + 2 * vb + sizeof(double) * (size_t)a0 * n;
+                char* dp = inp + 3 * vb + sizeof(double) * (size_t)a0 * stride;
+                CUDA_TRY(cudaMemcpyAsync(dx, x0, cvb, cudaMemcpyHostToDevice, st));
+                CUDA_TRY(cudaMemcpyAsync(dl, lw, cvb, cudaMemcpyHostToDevice, st));
+                CUDA_TRY(cudaMemcpyAsync(du, up, cvb, cudaMemcpyHostToDevice, st));
+                if (cpb) CUDA_TRY(cudaMemcpyAsync(dp, prm, cpb, cudaMemcpyHostToDevice, st));
+                x0 = reinterpret_cast<const double*>(dx);
+                lw = reinterpret_cast<const double*>(dl);
+                up = reinterpret_cast<const double*>(du);
+                prm = cpb ? reinterpret_cast<const double*>(dp) : nullptr;
+            }
+            auto off = [&](auto* p, int64_t m) { return p ? p + a0 * m : p; };
+            OutPtrs o{off(ofull.x_star, n), off(ofull.f_star, 1), off(ofull.pg, 1), off(ofull.status, 1),
+                      off(ofull.iters, 1), off(ofull.cg, 1),    off(ofull.fev, 1), off(ofull.flops, 1),
+                      off(ofull.wall, 1)};
+            tbdev::KernelArgs a = make_args(b, np, cfg, ctx->fast_forward, x0, lw, up, prm, stride, cc, o);
+            CUDA_TRY(attach_ws(d, b->family, a));
+            if (ch == 0) CUDA_TRY(cudaEventRecord(d.ev[1], st));
+            CUDA_TRY(tbdev::launch_tron(b->family, a, st));
+            if (cc > 0) ++g_launches;
+            if (ch == nch - 1 && nch == 1) CUDA_TRY(cudaEventRecord(d.ev[2], st));
+            if (out_host && cc > 0) {
+                const int64_t h0 = g0;
+                auto cp = [&](void* dst, const void* src, size_t bytes) -> cudaError_t {
+                    if (!dst) return cudaSuccess;
+                    return cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, st);
+                };
+                CUDA_TRY(cp(r->x_star ? r->x_star + h0 * n : nullptr, o.x_star, sizeof(double) * cc * n));
+                CUDA_TRY(cp(r->f_star ? r->f_star + h0 : nullptr, o.f_star, sizeof(double) * cc));
+                CUDA_TRY(cp(r->pg_norm ? r->pg_norm + h0 : nullptr, o.pg, sizeof(double) * cc));
+                CUDA_TRY(cp(r->status ? r->status + h0 : nullptr, o.status, sizeof(int32_t) * cc));
+                CUDA_TRY(cp(r->iterations ? r->iterations + h0 : nullptr, o.iters, sizeof(int32_t) * cc));
+                CUDA_TRY(cp(r->cg_iterations ? r->cg_iterations + h0 : nullptr, o.cg, sizeof(int64_t) * cc));
+                CUDA_TRY(cp(r->f_evals ? r->f_evals + h0 : nullptr, o.fev, sizeof(int64_t) * cc));
+                CUDA_TRY(cp(r->flops ? r->flops + h0 : nullptr, o.flops, sizeof(int64_t) * cc));
+                CUDA_TRY(cp(r->wall_time ? r->wall_time + h0 : nullptr, o.wall, sizeof(double) * cc));
+            }
+        }
+        if (nch > 1) {  // join the chunk streams back into the partition's stream
+            for (int ch = 0; ch < nch; ++ch) {
+                CUDA_TRY(cudaEventRecord(d.join, d.aux[ch]));
+                CUDA_TRY(cudaStreamWaitEvent(d.stream, d.join, 0));
+            }
+            CUDA_TRY(cudaEventRecord(d.ev[2], d.stream));  // chunked: includes the last D2H
         }
         CUDA_TRY(cudaEventRecord(d.ev[3], d.stream));
     }

@@ -93,6 +93,9 @@ struct Blk {
     int nf;
     long long fl;
     double extrap;
+#ifdef TB_PHASES
+    long long ph[16];
+#endif
 
     __device__ __forceinline__ void count(long long v) {
         if (COUNT) fl += v;
@@ -410,7 +413,10 @@ struct Blk {
         double alpha = 0.0;
 #pragma unroll 1
         for (;;) {
-            if (chol_attempt(alpha)) {
+            TB_PH_BEGIN(11)
+            const bool ok = chol_attempt(alpha);
+            TB_PH_END(*this, 11)
+            if (ok) {
                 shift = alpha;
                 if (t < nf) RD[t] = 1.0 / Lat(t, t);
                 sync();
@@ -498,9 +504,15 @@ struct Blk {
 #pragma unroll 1
         for (int k = 1; k <= nf; ++k) {
             iters = k;
+            TB_PH_BEGIN(9)
             const double z = trsv_bwd(p);
+            TB_PH_END(*this, 9)
+            TB_PH_BEGIN(10)
             double q = gemv_c(z);
+            TB_PH_END(*this, 10)
+            TB_PH_BEGIN(8)
             q = trsv_fwd(q);
+            TB_PH_END(*this, 8)
             count(2 * nf2);
             const double ptq = dot(p, q, C);
             double sigma;
@@ -637,7 +649,9 @@ struct Blk {
             build_free_set(fr);
             if (nf == 0) break;
             double shift;
+            TB_PH_BEGIN(2)
             int rc = ccf(shift);
+            TB_PH_END(*this, 2)
             if (rc) return rc;
             if (any(t < nf && Lat(t, t) == 0.0)) return TB_STATUS_SINGULAR_FACTOR;
             const double gfree = w + g;
@@ -645,11 +659,15 @@ struct Blk {
             const double gfnorm = nrm2(g, fset);
             double step_c;
             int cgs, its;
+            TB_PH_BEGIN(3)
             rc = precond_cg(to_c(gfree), delta, step_c, cgs, its);
+            TB_PH_END(*this, 3)
             if (rc) return rc;
             cg_total += its;
             const double step = to_o(step_c);
+            TB_PH_BEGIN(4)
             const double xn = line_search(xout, l, u, gfree, step);
+            TB_PH_END(*this, 4)
             if (fr) {
                 s += xn - xout;
                 xout = xn;
@@ -789,6 +807,10 @@ __global__ void __launch_bounds__(D, BlkMinBlocks<D>::value) tron_block_kernel(c
         if (pid >= a.count) break;
         const unsigned long long t_start = globaltimer();
         W.fl = 0;
+#ifdef TB_PHASES
+        for (int k = 0; k < 16; ++k) W.ph[k] = 0;
+        const long long tb_ph_total0 = clock64();
+#endif
         W.prm = a.prm ? a.prm + pid * a.stride : nullptr;
         BlkFamily<FAM, D, ASMEM, COUNT> fam;
         const double l = act ? a.lo[pid * n + t] : 0.0;
@@ -812,8 +834,10 @@ __global__ void __launch_bounds__(D, BlkMinBlocks<D>::value) tron_block_kernel(c
             double delta_in = 0.0, alpha_in = 0.0;
 #pragma unroll 1
             for (int iter = 0;; ++iter) {
+                TB_PH_BEGIN(6)
                 fam.prepare(W, xe);
                 const double fe = fam.f(W);
+                TB_PH_END(W, 6)
                 W.count(tb_family_flops(FAM, n, 0));
                 ++f_evals;
                 bool take = iter == 0;
@@ -877,7 +901,9 @@ __global__ void __launch_bounds__(D, BlkMinBlocks<D>::value) tron_block_kernel(c
                 if (iter + 1 > cfg.max_iter) break;
                 iterations = iter + 1;
                 if (need_hessian) {
+                    TB_PH_BEGIN(0)
                     fam.hess(W);
+                    TB_PH_END(W, 0)
                     W.count(tb_family_flops(FAM, n, 2));
                     need_hessian = false;
                 }
@@ -885,13 +911,17 @@ __global__ void __launch_bounds__(D, BlkMinBlocks<D>::value) tron_block_kernel(c
                 delta_in = delta;
                 alpha_in = alpha_c;
                 double cs, alpha_new;
+                TB_PH_BEGIN(1)
                 int rc = W.cauchy(x, g, l, u, delta, alpha_c, alpha_new, cs);
+                TB_PH_END(W, 1)
                 if (rc) {
                     status = rc;
                     break;
                 }
                 alpha_c = alpha_new;
+                TB_PH_BEGIN(5)
                 rc = W.subspace_step(x, g, l, u, delta, cs, xe, s, cg_its);
+                TB_PH_END(W, 5)
                 if (rc) {
                     status = rc;
                     break;
@@ -899,6 +929,11 @@ __global__ void __launch_bounds__(D, BlkMinBlocks<D>::value) tron_block_kernel(c
                 cg_iterations += cg_its;
             }
         }
+#ifdef TB_PHASES
+        W.ph[7] = clock64() - tb_ph_total0;
+        if (t == 0)
+            for (int k = 0; k < 16; ++k) atomicAdd(&g_phase_cycles[k], (unsigned long long)W.ph[k]);
+#endif
         if (act && a.x_star) a.x_star[pid * n + t] = x;
         if (t == 0) {
             if (a.f_star) a.f_star[pid] = f;

@@ -62,7 +62,7 @@
 namespace tbdev {
 
 #ifdef TB_PHASES
-__device__ unsigned long long g_phase_cycles[8];
+__device__ unsigned long long g_phase_cycles[16];
 #endif
 
 constexpr unsigned FULL = 0xffffffffu;

@@ -22,8 +22,8 @@ cudaError_t ws_need_hs45(int n, long long count, size_t* bytes) {
 #ifdef TB_PHASES
 // debug build only: per-phase cycle totals of this family's kernels
 extern "C" int tb_debug_read_phases_hs45(unsigned long long* out) {
-    if (cudaMemcpyFromSymbol(out, tbdev::g_phase_cycles, sizeof(unsigned long long) * 8) != cudaSuccess) return 2;
-    unsigned long long z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    if (cudaMemcpyFromSymbol(out, tbdev::g_phase_cycles, sizeof(unsigned long long) * 16) != cudaSuccess) return 2;
+    unsigned long long z[16] = {};
     return cudaMemcpyToSymbol(tbdev::g_phase_cycles, z, sizeof z) == cudaSuccess ? 0 : 2;
 }
 #endif

@@ -7,11 +7,12 @@ from paper_2106_14995_b200 import Solver, _lib, synth
 
 fam, n = sys.argv[1], int(sys.argv[2])
 name = fam.rstrip("0123456789"); dim = int(fam[len(name):])
+name = {"branch": "branch"}.get(name, name)
 b = synth.make(name, n, dim)
 s = Solver((0,))
 lib = _lib.load()
 rd = getattr(lib, f"tb_debug_read_phases_{name}")
-buf = (C.c_ulonglong * 8)()
+buf = (C.c_ulonglong * 16)()
 s.solve_batch(b); rd(buf)
 r = s.solve_batch(b); rd(buf)
 ph = np.array(list(buf), dtype=np.float64)
@@ -24,3 +25,7 @@ print(f"{fam} x{n}: kernel {r.kernel_time*1e3:.3f} ms; mean warp cycles/solve {t
 for k, v in [("hessian", ph[0]), ("cauchy", ph[1]), ("ccf", ph[2]), ("pcg", ph[3]), ("line_search", ph[4]),
              ("subspace other", sub_other), ("f_eval+prepare", ph[6]), ("rest (grad, radius, setup)", rest)]:
     print(f"  {k:28s} {100*v/tot:5.1f}%  {v/n:10,.0f} cycles/solve")
+if ph[8] + ph[9] + ph[10] + ph[11] > 0:  # block kernel (d > 32) breakdown
+    for k, v in [("  pcg: trsv_fwd (loop)", ph[8]), ("  pcg: trsv_bwd (loop)", ph[9]), ("  pcg: gemv_c", ph[10]),
+                 ("  ccf: chol attempts", ph[11])]:
+        print(f"  {k:28s} {100*v/tot:5.1f}%  {v/n:10,.0f} cycles/solve")
