@@ -50,15 +50,15 @@ struct BlkLayout {
     static constexpr int S3 = S2 + 2 * D;
     static constexpr int BB = S3 + 2 * D;            // triangular-solve results
     static constexpr int XS = BB + D;                // evaluation point
-    static constexpr int MISC = XS + D;              // 32 doubles of scalars
-    static constexpr int FIDX = MISC + 32;           // D int32: free index by rank
+    static constexpr int MISC = XS + D;              // 40 doubles of scalars (BM_*)
+    static constexpr int FIDX = MISC + 40;           // D int32: free index by rank
     static constexpr int MSK = FIDX + D / 2;         // 2 x NW uint32 ballot words
     static constexpr int AS = MSK + ((NW + 1) & ~1); // Hessian (ASMEM only)
     static constexpr int total() { return AS + (ASMEM ? D * D : 0); }
     static_assert(LP % 2 == 0, "alignment");
 };
 // MISC slots
-enum { BM_PIV = 0, BM_NXT = 2, BM_RED = 4, BM_PID = 30 };
+enum { BM_RED = 0, BM_PID = 16, BM_GOK = 18, BM_GFL = 20, BM_GRP = 24, BM_MISC_SIZE = 40 };
 
 // a subset of the variables: its size and this thread's ascending rank in it
 // (-1 if absent).  The staged vector of a subset is indexed by rank.
@@ -72,7 +72,8 @@ struct Blk {
     using SL = BlkLayout<D, ASMEM>;
     static constexpr int NW = SL::NW;
     double* A;       // D x D column-major (shared or global workspace)
-    double* L;       // packed lower factor of the current free system
+    double* L;       // packed lower factors, one per attempt group
+    double* Lw;      // the successful attempt's factor
     double* RD;
     double* s1;
     double* s2;
@@ -103,7 +104,7 @@ struct Blk {
     __device__ __forceinline__ void sync() { __syncthreads(); }
     __device__ __forceinline__ bool any(bool p) { return __syncthreads_or(p) != 0; }
     __device__ __forceinline__ int cs(int q) const { return q * nf - (q * (q - 1)) / 2; }  // packed column start
-    __device__ __forceinline__ double& Lat(int i, int q) { return L[cs(q) + (i - q)]; }
+    __device__ __forceinline__ double& Lat(int i, int q) { return Lw[cs(q) + (i - q)]; }
 
     // ------------------------------------------------ ordered reductions
     __device__ __forceinline__ static double dense_sum(const double* b, int cnt) {
@@ -333,17 +334,29 @@ struct Blk {
     }
 
     // ------------------------------------------------ dense.hpp factorization
-    // cholesky_left_looking (dense.hpp:138-156) on B = A[F,F] with shift sh.
-    // Thread p computes L(p, j) for column j; the division by d of column j
-    // is applied at the start of column j + 1 (one barrier per column).
-    __device__ __forceinline__ bool chol_attempt(double sh) {
-        const int p = t;
+    // Shift escalation in parallel (dense.hpp:182-201), like the warp
+    // kernel: the reference tries A + a_k I for a_0 = 0, a_{k+1} =
+    // max(2 a_k, alpha0) until one factorization succeeds.  Attempts are
+    // independent, so the block splits into G groups of GT threads (GT = 32,
+    // 64 or 128 >= nf), each running attempt k0 + g on its own packed factor;
+    // the first success in k order is the reference's result.  Groups
+    // synchronise with __syncwarp (GT = 32) or a named barrier.
+    __device__ __forceinline__ void gsync(int gid, int gt) {
+        if (gt == 32) __syncwarp();
+        else if (gt == D) __syncthreads();
+        else asm volatile("bar.sync %0, %1;" ::"r"(1 + gid), "r"(gt) : "memory");
+    }
+
+    // cholesky_left_looking (dense.hpp:138-156) on B = A[F,F] + sh I by one
+    // group: thread p computes L(p, j) of column j; the division by d of
+    // column j is applied at the start of column j + 1 (one barrier per column).
+    __device__ __forceinline__ bool chol_attempt(double sh, double* Lg, double* slot, int p, int gid, int gt,
+                                                 long long& fla) {
         const bool rowv = p < nf;
         const double* Ar = A + (rowv ? fidx[p] : 0);
-        double* piv = misc + BM_PIV;
-        double* nxt = misc + BM_NXT;
+        double* piv = slot;      // [2]
+        double* nxt = slot + 2;  // [2]
         double own_prev = 0.0, dprev = 1.0;
-        long long fla = 0;
 #pragma unroll 1
         for (int j = 0; j < nf; ++j) {
             const bool row = rowv && p >= j;
@@ -352,19 +365,20 @@ struct Blk {
                 ljprev = nxt[(j - 1) & 1] / dprev;
                 if (row) {
                     own_prev = own_prev / dprev;  // L(p, j-1)
-                    Lat(p, j - 1) = own_prev;
+                    Lg[cs(j - 1) + p - (j - 1)] = own_prev;
                 }
             }
             double lij = row ? Ar[fidx[j] * D] : 0.0;
             if (p == j) lij += sh;
             int cnt = 0;
-            const double* Lj = L + j;  // L(j, k) = Lj[cs(k) - k]
+            const double* Lj = Lg + j;  // L(j, k) = Lj[cs(k) - k]
 #pragma unroll 4
             for (int k = 0; k < j - 1; ++k) {
                 const int c = cs(k) - k;
                 const double ljk = Lj[c];
+                const double lpk = Lg[c + (row ? p : j)];
                 if (ljk != 0.0) {
-                    if (row) lij -= ljk * L[c + p];
+                    if (row) lij -= ljk * lpk;
                     ++cnt;
                 }
             }
@@ -374,26 +388,21 @@ struct Blk {
             }
             if (p == j) piv[j & 1] = lij;
             if (p == j + 1) nxt[j & 1] = lij;
-            sync();
+            gsync(gid, gt);
             const double pivot = piv[j & 1];
             const bool ok = pivot > 0.0;
             if (COUNT) fla += 1 + 2LL * (nf - j) * cnt + (ok ? nf - j : 0);
-            if (!ok) {
-                count(fla);
-                sync();  // piv[] is rewritten by the next attempt
-                return false;
-            }
+            if (!ok) return false;
             const double d = sqrt(pivot);
-            if (p == j) Lat(j, j) = d;
+            if (p == j) Lg[cs(j)] = d;
             own_prev = lij;
             dprev = d;
         }
-        count(fla);
-        sync();
         return true;
     }
 
-    // dense.hpp:182-201 shifted_factorize on B.  Returns 0 or FACTORIZATION_FAILED.
+    // dense.hpp:182-201 shifted_factorize on B.  On success Lw is the factor
+    // and RD its reciprocal diagonal.  Returns 0 or FACTORIZATION_FAILED.
     __device__ __forceinline__ int ccf(double& shift) {
         double dg = 0.0, ma = 0.0;
         if (t < nf) {
@@ -410,21 +419,57 @@ struct Blk {
         const double max_abs = bmax_nonneg(ma);
         const double alpha0 = tb_smax(1e-3 * max_diag, 1e-8);
         const double cap = 1e8 * tb_smax(1.0, max_abs);
-        double alpha = 0.0;
+        const int gt = nf <= 32 ? 32 : (nf <= 64 && D > 64 ? 64 : D);
+        const int G = D / gt;
+        const int gid = t / gt, p = t % gt;
+        const int lpg = ((nf * (nf + 1)) / 2 + 1) & ~1;
+        double* Lg = L + gid * lpg;
+        int* gok = reinterpret_cast<int*>(misc + BM_GOK);
+        long long* gfl = reinterpret_cast<long long*>(misc + BM_GFL);
+        double base = 0.0;  // a_{k0}
 #pragma unroll 1
-        for (;;) {
-            TB_PH_BEGIN(11)
-            const bool ok = chol_attempt(alpha);
-            TB_PH_END(*this, 11)
-            if (ok) {
-                shift = alpha;
+        for (int k0 = 0;; k0 += G) {
+            double sh = base;
+            for (int q = 0; q < gid; ++q) sh = tb_smax(2.0 * sh, alpha0);
+            const bool valid = (k0 + gid == 0) || (sh <= cap);
+            long long fla = 0;
+            bool ok = false;
+            if (valid) {
+                TB_PH_BEGIN(11)
+                ok = chol_attempt(sh, Lg, misc + BM_GRP + 4 * gid, p, gid, gt, fla);
+                TB_PH_END(*this, 11)
+            }
+            if (p == 0) {
+                gok[gid] = ok ? 1 : (valid ? 0 : -1);
+                if (COUNT) gfl[gid] = fla;
+            }
+            sync();
+            int winner = -1;
+            bool all_valid = true;
+            for (int q = 0; q < G; ++q) {
+                const int v = gok[q];
+                if (v == 1 && winner < 0) winner = q;
+                if (v < 0) all_valid = false;
+            }
+            if (COUNT) {
+                const int last = winner >= 0 ? winner : G - 1;
+                for (int q = 0; q <= last; ++q)
+                    if (gok[q] >= 0) count(gfl[q] + ((q < winner || winner < 0) ? 1 : 0));
+            }
+            if (winner >= 0) {
+                double sw = base;
+                for (int q = 0; q < winner; ++q) sw = tb_smax(2.0 * sw, alpha0);
+                shift = sw;
+                Lw = L + winner * lpg;
                 if (t < nf) RD[t] = 1.0 / Lat(t, t);
                 sync();
                 return 0;
             }
-            alpha = tb_smax(2.0 * alpha, alpha0);
-            count(1);
-            if (!(alpha <= cap)) return TB_STATUS_FACTORIZATION_FAILED;
+            // no success among attempts k0..k0+G-1: the reference throws at
+            // the first a_k > cap (all earlier attempts failed)
+            if (!all_valid) return TB_STATUS_FACTORIZATION_FAILED;
+            for (int q = 0; q < G; ++q) base = tb_smax(2.0 * base, alpha0);
+            sync();  // gok / group slots are rewritten by the next round
         }
     }
 
@@ -456,7 +501,7 @@ struct Blk {
             double last = 0.0;
 #pragma unroll 1
             for (int i = nf - 1; i >= 0; --i) {
-                const double* Lc = L + cs(i) - i;  // L(j, i) = Lc[j]
+                const double* Lc = Lw + cs(i) - i;  // L(j, i) = Lc[j]
                 double s = in[i];
                 if (i + 1 < nf) s -= Lc[i + 1] * last;
                 int j = i + 2;
@@ -776,6 +821,7 @@ __global__ void __launch_bounds__(D, BlkMinBlocks<D>::value) tron_block_kernel(c
     W.A = ASMEM ? smem + SL::AS
                 : reinterpret_cast<double*>(static_cast<char*>(a.ws) + kBlkWsHeader) + (size_t)blockIdx.x * D * D;
     W.L = smem + SL::L;
+    W.Lw = W.L;
     W.RD = smem + SL::RD;
     W.s1 = smem + SL::S1;
     W.s2 = smem + SL::S2;
