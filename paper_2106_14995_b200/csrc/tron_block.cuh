@@ -50,15 +50,15 @@ struct BlkLayout {
     static constexpr int S3 = S2 + 2 * D;
     static constexpr int BB = S3 + 2 * D;            // triangular-solve results
     static constexpr int XS = BB + D;                // evaluation point
-    static constexpr int MISC = XS + D;              // 40 doubles of scalars (BM_*)
-    static constexpr int FIDX = MISC + 40;           // D int32: free index by rank
+    static constexpr int MISC = XS + D;              // 48 doubles of scalars (BM_*)
+    static constexpr int FIDX = MISC + 48;           // D int32: free index by rank
     static constexpr int MSK = FIDX + D / 2;         // 2 x NW uint32 ballot words
     static constexpr int AS = MSK + ((NW + 1) & ~1); // Hessian (ASMEM only)
     static constexpr int total() { return AS + (ASMEM ? D * D : 0); }
     static_assert(LP % 2 == 0, "alignment");
 };
 // MISC slots
-enum { BM_RED = 0, BM_PID = 16, BM_GOK = 18, BM_GFL = 20, BM_GRP = 24, BM_MISC_SIZE = 40 };
+enum { BM_RED = 0, BM_PID = 16, BM_GOK = 18, BM_GFL = 20, BM_GRP = 24, BM_PCG = 40, BM_MISC_SIZE = 48 };
 
 // a subset of the variables: its size and this thread's ascending rank in it
 // (-1 if absent).  The staged vector of a subset is indexed by rank.
@@ -88,6 +88,7 @@ struct Blk {
     int n;
     int t;       // thread index == owned variable
     int tog;     // staging toggle (0 or D); also selects ballot / reduction slots
+    int wtog;    // staging toggle of the warp-level PCG (0 or 32)
     BSet act;    // all n variables
     BSet fset;   // current free set, original ownership (rank of variable t)
     BSet cset;   // current free set, compacted ownership (thread p owns rank p)
@@ -350,41 +351,53 @@ struct Blk {
     // cholesky_left_looking (dense.hpp:138-156) on B = A[F,F] + sh I by one
     // group: thread p computes L(p, j) of column j; the division by d of
     // column j is applied at the start of column j + 1 (one barrier per column).
-    __device__ __forceinline__ bool chol_attempt(double sh, double* Lg, double* slot, int p, int gid, int gt,
-                                                 long long& fla) {
+    __device__ __forceinline__ bool chol_attempt(double sh, double* Lg, const double* Bs, double* slot, int p,
+                                                 int gid, int gt, long long& fla) {
         const bool rowv = p < nf;
         const double* Ar = A + (rowv ? fidx[p] : 0);
         double* piv = slot;      // [2]
         double* nxt = slot + 2;  // [2]
-        double own_prev = 0.0, dprev = 1.0;
+        double own_prev = 0.0, dprev = 1.0, rprev = 1.0;  // rprev = RN(1 / dprev)
+        int csj = 0;                                         // cs(j)
 #pragma unroll 1
         for (int j = 0; j < nf; ++j) {
             const bool row = rowv && p >= j;
-            double ljprev = 0.0;  // L(j, j-1)
-            if (j > 0) {
-                ljprev = nxt[(j - 1) & 1] / dprev;
-                if (row) {
-                    own_prev = own_prev / dprev;  // L(p, j-1)
-                    Lg[cs(j - 1) + p - (j - 1)] = own_prev;
-                }
-            }
-            double lij = row ? Ar[fidx[j] * D] : 0.0;
+            const int pr = row ? p : j;  // row read by this thread (any valid row if idle)
+            double lij = row ? (Bs ? Bs[csj + p - j] : Ar[fidx[j] * D]) : 0.0;
             if (p == j) lij += sh;
             int cnt = 0;
-            const double* Lj = Lg + j;  // L(j, k) = Lj[cs(k) - k]
-#pragma unroll 4
-            for (int k = 0; k < j - 1; ++k) {
-                const int c = cs(k) - k;
-                const double ljk = Lj[c];
-                const double lpk = Lg[c + (row ? p : j)];
-                if (ljk != 0.0) {
-                    if (row) lij -= ljk * lpk;
+            // terms k = 0 .. j-2 (already normalised), ascending; loads first
+            const double* Lj = Lg + j;  // L(j, k) = Lj[c_k], c_k = cs(k) - k
+            int c = 0, k = 0;
+#pragma unroll 1
+            for (; k + 4 <= j - 1; k += 4) {
+                const int c1 = c + nf - k - 1, c2 = c1 + nf - k - 2, c3 = c2 + nf - k - 3;
+                const double l0 = Lj[c], l1 = Lj[c1], l2 = Lj[c2], l3 = Lj[c3];
+                const double q0 = Lg[c + pr], q1 = Lg[c1 + pr], q2 = Lg[c2 + pr], q3 = Lg[c3 + pr];
+                if (l0 != 0.0) { if (row) lij -= l0 * q0; ++cnt; }
+                if (l1 != 0.0) { if (row) lij -= l1 * q1; ++cnt; }
+                if (l2 != 0.0) { if (row) lij -= l2 * q2; ++cnt; }
+                if (l3 != 0.0) { if (row) lij -= l3 * q3; ++cnt; }
+                c = c3 + nf - k - 4;
+            }
+#pragma unroll 1
+            for (; k < j - 1; ++k) {
+                const double l0 = Lj[c], q0 = Lg[c + pr];
+                if (l0 != 0.0) { if (row) lij -= l0 * q0; ++cnt; }
+                c += nf - k - 1;
+            }
+            // term k = j-1: L(j, j-1) and L(p, j-1) are the quotients of the
+            // raw values by d_{j-1} (IEEE, via the correctly rounded reciprocal)
+            if (j > 0) {
+                const double ljprev = div_rcp(nxt[(j - 1) & 1], dprev, rprev);
+                if (row) {
+                    own_prev = div_rcp(own_prev, dprev, rprev);
+                    Lg[c + p] = own_prev;  // c == cs(j-1) - (j-1)
+                }
+                if (ljprev != 0.0) {
+                    if (row) lij -= ljprev * own_prev;
                     ++cnt;
                 }
-            }
-            if (j > 0 && ljprev != 0.0) {
-                if (row) lij -= ljprev * own_prev;
-                ++cnt;
             }
             if (p == j) piv[j & 1] = lij;
             if (p == j + 1) nxt[j & 1] = lij;
@@ -394,9 +407,11 @@ struct Blk {
             if (COUNT) fla += 1 + 2LL * (nf - j) * cnt + (ok ? nf - j : 0);
             if (!ok) return false;
             const double d = sqrt(pivot);
-            if (p == j) Lg[cs(j)] = d;
+            if (p == j) Lg[csj] = d;
             own_prev = lij;
             dprev = d;
+            rprev = 1.0 / d;
+            csj += nf - j;
         }
         return true;
     }
@@ -404,6 +419,14 @@ struct Blk {
     // dense.hpp:182-201 shifted_factorize on B.  On success Lw is the factor
     // and RD its reciprocal diagonal.  Returns 0 or FACTORIZATION_FAILED.
     __device__ __forceinline__ int ccf(double& shift) {
+        const int gt = nf <= 32 ? 32 : (nf <= 64 && D > 64 ? 64 : D);
+        const int G = D / gt;
+        const int gid = t / gt, p = t % gt;
+        const int lpg = ((nf * (nf + 1)) / 2 + 1) & ~1;
+        double* Lg = L + gid * lpg;
+        // B = A[F,F] (lower triangle) staged once per call behind the G
+        // factors when it fits: every attempt then reads shared memory
+        double* Bs = (G + 1) * lpg <= SL::LP ? L + G * lpg : nullptr;
         double dg = 0.0, ma = 0.0;
         if (t < nf) {
             const double* Ar = A + fidx[t];
@@ -411,7 +434,9 @@ struct Blk {
             if (isnan(dg)) dg = 0.0;
 #pragma unroll 4
             for (int q = 0; q < nf; ++q) {
-                const double v = fabs(Ar[fidx[q] * D]);
+                const double a = Ar[fidx[q] * D];
+                if (Bs && q <= t) Bs[cs(q) + t - q] = a;
+                const double v = fabs(a);
                 if (!isnan(v)) ma = fmax(ma, v);
             }
         }
@@ -419,11 +444,6 @@ struct Blk {
         const double max_abs = bmax_nonneg(ma);
         const double alpha0 = tb_smax(1e-3 * max_diag, 1e-8);
         const double cap = 1e8 * tb_smax(1.0, max_abs);
-        const int gt = nf <= 32 ? 32 : (nf <= 64 && D > 64 ? 64 : D);
-        const int G = D / gt;
-        const int gid = t / gt, p = t % gt;
-        const int lpg = ((nf * (nf + 1)) / 2 + 1) & ~1;
-        double* Lg = L + gid * lpg;
         int* gok = reinterpret_cast<int*>(misc + BM_GOK);
         long long* gfl = reinterpret_cast<long long*>(misc + BM_GFL);
         double base = 0.0;  // a_{k0}
@@ -436,7 +456,7 @@ struct Blk {
             bool ok = false;
             if (valid) {
                 TB_PH_BEGIN(11)
-                ok = chol_attempt(sh, Lg, misc + BM_GRP + 4 * gid, p, gid, gt, fla);
+                ok = chol_attempt(sh, Lg, Bs, misc + BM_GRP + 4 * gid, p, gid, gt, fla);
                 TB_PH_END(*this, 11)
             }
             if (p == 0) {
@@ -497,34 +517,184 @@ struct Blk {
         tog ^= D;
         if (t < nf) in[t] = b;
         sync();
-        if (t < 32) {
-            double last = 0.0;
-#pragma unroll 1
-            for (int i = nf - 1; i >= 0; --i) {
-                const double* Lc = Lw + cs(i) - i;  // L(j, i) = Lc[j]
-                double s = in[i];
-                if (i + 1 < nf) s -= Lc[i + 1] * last;
-                int j = i + 2;
-#pragma unroll 1
-                for (; j + 4 <= nf; j += 4) {
-                    const double p0 = Lc[j] * bb[j];
-                    const double p1 = Lc[j + 1] * bb[j + 1];
-                    const double p2 = Lc[j + 2] * bb[j + 2];
-                    const double p3 = Lc[j + 3] * bb[j + 3];
-                    s -= p0;
-                    s -= p1;
-                    s -= p2;
-                    s -= p3;
-                }
-#pragma unroll 1
-                for (; j < nf; ++j) s -= Lc[j] * bb[j];
-                last = div_rcp(s, Lc[i], RD[i]);
-                if (t == 0) bb[i] = last;
-                __syncwarp();
-            }
-        }
+        if (t < 32) bwd_core(in);
         sync();
         return t < nf ? bb[t] : 0.0;
+    }
+    // the serial backward recurrence, run by warp 0 (lanes compute the same
+    // values); results in bb[0..nf-1]
+    __device__ __forceinline__ void bwd_core(const double* in) {
+        double last = 0.0;
+#pragma unroll 1
+        for (int i = nf - 1; i >= 0; --i) {
+            const double* Lc = Lw + cs(i) - i;  // L(j, i) = Lc[j]
+            double s = in[i];
+            if (i + 1 < nf) s -= Lc[i + 1] * last;
+            int j = i + 2;
+#pragma unroll 1
+            for (; j + 4 <= nf; j += 4) {
+                const double p0 = Lc[j] * bb[j];
+                const double p1 = Lc[j + 1] * bb[j + 1];
+                const double p2 = Lc[j + 2] * bb[j + 2];
+                const double p3 = Lc[j + 3] * bb[j + 3];
+                s -= p0;
+                s -= p1;
+                s -= p2;
+                s -= p3;
+            }
+#pragma unroll 1
+            for (; j < nf; ++j) s -= Lc[j] * bb[j];
+            last = div_rcp(s, Lc[i], RD[i]);
+            if (t == 0) bb[i] = last;
+            __syncwarp();
+        }
+    }
+
+    // ---------------------------------- warp-level PCG pieces (nf <= 32)
+    // Run by warp 0 only (lane p owns free rank p); shuffles and __syncwarp,
+    // no block barrier.  Same operations in the same order as the block forms.
+    // Staging (s1, s2, s3 are idle while the other warps wait): s1[0,64) sums,
+    // s2[0,64) / s3[0,64) the 2nd / 3rd sums, s2[64,128) backward-solve input,
+    // s3[64,128) gemv input; each toggled by wtog.
+    __device__ __forceinline__ double wsum(double v) {
+        double* b = s1 + wtog;
+        wtog ^= 32;
+        if (t < nf) b[t] = v;
+        __syncwarp();
+        return dense_sum(b, nf);
+    }
+    __device__ __forceinline__ void wsum3(double a, double c, double e, double& sa, double& sc, double& se) {
+        double* b = s1 + wtog;
+        double* b2 = s2 + wtog;
+        double* b3 = s3 + wtog;
+        wtog ^= 32;
+        if (t < nf) {
+            b[t] = a;
+            b2[t] = c;
+            b3[t] = e;
+        }
+        __syncwarp();
+        sa = dense_sum(b, nf);
+        sc = dense_sum(b2, nf);
+        se = dense_sum(b3, nf);
+    }
+    __device__ __forceinline__ double wdot(double x, double y) {
+        count(2 * nf);
+        return wsum(x * y);
+    }
+    __device__ __forceinline__ double wtrsv_fwd(double b) {
+        const int p = t;
+        double s = p < nf ? b : 0.0;
+#pragma unroll 1
+        for (int j = 0; j < nf; ++j) {
+            const double q = div_rcp(__shfl_sync(FULL, s, j), Lat(j, j), RD[j]);
+            if (p == j) s = q;
+            else if (p > j && p < nf) s -= Lat(p, j) * q;
+        }
+        return s;
+    }
+    __device__ __forceinline__ double wtrsv_bwd(double b) {
+        double* in = s2 + 64 + wtog;
+        wtog ^= 32;
+        if (t < nf) in[t] = b;
+        __syncwarp();
+        bwd_core(in);
+        return t < nf ? bb[t] : 0.0;
+    }
+    __device__ __forceinline__ double wgemv_c(double z) {
+        double* b = s3 + 64 + wtog;
+        wtog ^= 32;
+        if (t < nf) b[t] = z;
+        __syncwarp();
+        double y = 0.0 * 0.0;
+        int u = 0;
+        if (t < nf) {
+            const double* Ar = A + fidx[t];
+#pragma unroll 4
+            for (int q = 0; q < nf; ++q) {
+                const double zq = 1.0 * b[q];
+                if (zq != 0.0) y += zq * Ar[fidx[q] * D];
+            }
+        }
+        if (COUNT) {
+            for (int q = 0; q < nf; ++q) u += (1.0 * b[q]) != 0.0;
+            fl += 2LL * nf * u;
+        }
+        return y;
+    }
+    __device__ __forceinline__ int wtrqsol(double x, double w, double delta, double& sigma) {
+        double ptx, ptp, xtx;
+        wsum3(w * x, w * w, x * x, ptx, ptp, xtx);
+        count(6 * nf + 8);
+        if (ptp == 0.0) return TB_STATUS_ZERO_DIRECTION;
+        const double dsq = delta * delta;
+        const double rad = sqrt(tb_smax(ptx * ptx + ptp * tb_smax(dsq - xtx, 0.0), 0.0));
+        if (ptx > 0.0) sigma = (dsq - xtx) / (ptx + rad);
+        else sigma = (rad - ptx) / ptp;
+        return 0;
+    }
+    // tron.hpp:290-344 on warp 0
+    __device__ __forceinline__ int precond_cg_w(double gfree, double delta, double& step, int& cg_status,
+                                                int& iters) {
+        const long long nf2 = (long long)nf * nf;
+        double w = 0.0;
+        count(nf);
+        const double bhat = wtrsv_fwd(gfree * -1.0);
+        count(nf2);
+        count(1);
+        const double bnorm = sqrt(wdot(bhat, bhat));
+        iters = 0;
+        if (bnorm == 0.0) {
+            step = 0.0;
+            cg_status = 0;
+            return 0;
+        }
+        double r = bhat, p = r;
+        double rho = wdot(r, r);
+        cg_status = 3;
+#pragma unroll 1
+        for (int k = 1; k <= nf; ++k) {
+            iters = k;
+            const double z = wtrsv_bwd(p);
+            double q = wgemv_c(z);
+            q = wtrsv_fwd(q);
+            count(2 * nf2);
+            const double ptq = wdot(p, q);
+            double sigma;
+            const int rc = wtrqsol(w, p, delta, sigma);
+            if (rc) return rc;
+            if (ptq <= 0.0) {
+                w += sigma * p;
+                count(2 * nf);
+                cg_status = 2;
+                break;
+            }
+            const double alpha = rho / ptq;
+            count(1);
+            if (alpha >= sigma) {
+                w += sigma * p;
+                count(2 * nf);
+                cg_status = 1;
+                break;
+            }
+            w += alpha * p;
+            r += (-alpha) * q;
+            count(4 * nf);
+            const double rtr = wdot(r, r);
+            count(2);
+            if (sqrt(rtr) <= cfg->cg_tol * bnorm) {
+                cg_status = 0;
+                break;
+            }
+            const double beta = rtr / rho;
+            p = beta * p;
+            p += 1.0 * r;
+            count(3 * nf + 1);
+            rho = rtr;
+        }
+        step = wtrsv_bwd(w);
+        count(nf2);
+        return 0;
     }
 
     // ------------------------------------------------ tron.hpp:290-344
@@ -705,7 +875,24 @@ struct Blk {
             double step_c;
             int cgs, its;
             TB_PH_BEGIN(3)
-            rc = precond_cg(to_c(gfree), delta, step_c, cgs, its);
+            const double gc = to_c(gfree);
+            if (nf <= 32) {  // warp 0 alone, no block barriers
+                int* res = reinterpret_cast<int*>(misc + BM_PCG);
+                if (t < 32) {
+                    rc = precond_cg_w(gc, delta, step_c, cgs, its);
+                    if (t == 0) {
+                        res[0] = rc;
+                        res[1] = cgs;
+                        res[2] = its;
+                    }
+                }
+                sync();
+                rc = res[0];
+                cgs = res[1];
+                its = res[2];
+            } else {
+                rc = precond_cg(gc, delta, step_c, cgs, its);
+            }
             TB_PH_END(*this, 3)
             if (rc) return rc;
             cg_total += its;
@@ -836,6 +1023,7 @@ __global__ void __launch_bounds__(D, BlkMinBlocks<D>::value) tron_block_kernel(c
     W.n = a.n;
     W.t = threadIdx.x;
     W.tog = 0;
+    W.wtog = 0;
     W.nf = 0;
     const int n = a.n;
     const int t = W.t;
