@@ -224,6 +224,63 @@ def run_admm(args, rank, world, local, dev):
     return line
 
 
+C3_DIMS = (4, 8, 16, 32, 64, 128)
+C3_BATCH = 32768
+
+
+def run_sweep(args, dev):
+    """C1 (1,024 ncvx d=4) and the C3 dimension sweep (ncvx, batch 32,768,
+    d = 4..128): device time of one batched solve with inputs in HBM (median
+    of `reps` after a warm-up) next to the reference's CPU solve_batch on a
+    bounded sample (all host threads).  Parity for these shapes is covered by
+    tests/test_gpu_parity.py (bitwise); this reports speed only."""
+    import torch
+
+    from paper_2106_14995_b200 import ProblemBatch, Solver, synth
+
+    solver = Solver((dev.index,))
+    t = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(dev)  # noqa: E731
+    cores = os.cpu_count() or 1
+    have_ref = False
+    try:
+        from oracle import pyoracle
+
+        have_ref = pyoracle.ref_available() and not args.no_cpu_baseline
+    except Exception:
+        pass
+    out = []
+    cases = [("C1", 1024, 4, 1)] + [("C3", C3_BATCH, d, 3 + d) for d in C3_DIMS]
+    for name, B, d, seed in cases:
+        b = synth.ncvx(B, d, seed=seed)
+        db = ProblemBatch(b.family, d, t(b.lower), t(b.upper), t(b.params), t(b.x0))
+        out_d = Solver.alloc_result(B, d, device=True)
+        solver.solve_batch(db, out=out_d)
+        reps = 3 if d <= 64 else 2
+        ks = []
+        for _ in range(reps):
+            solver.solve_batch(db, out=out_d)
+            ks.append(out_d.kernel_time)
+        ms = 1e3 * statistics.median(ks)
+        row = {"config": name, "family": "ncvx", "dim": d, "batch": B, "ms": ms, "solves_per_s": B / (ms * 1e-3),
+               "kernel": "warp per problem" if d <= 32 else f"block of {64 if d <= 64 else 128} threads (persistent)",
+               "mean_iterations": float(out_d.iterations.double().mean().item()),
+               "status_counts": {str(k): int(v) for k, v in
+                                 zip(*np.unique(out_d.status.cpu().numpy(), return_counts=True))}}
+        if have_ref:
+            guess = {4: 60000, 8: 20000, 16: 6000, 32: 2500, 64: 700, 128: 200}[d]  # per-thread solves/s
+            n = int(min(B, max(64, 1.0 * guess * cores)))
+            sub = ProblemBatch(b.family, d, b.lower[:n], b.upper[:n], b.params[:n], b.x0[:n])
+            v, _ = cpu_reference_run(sub, cores, reps=2)
+            row["cpu_baseline"] = {"value": v, "unit": "solves/s", "cores": cores, "kind": "reference",
+                                   "sample": f"first {n} of the {B} problems, reference solve_batch(workers={cores})"}
+            row["speedup_vs_cpu"] = row["solves_per_s"] / v
+        out.append(row)
+        del db, out_d, b
+        torch.cuda.empty_cache()
+    solver.close()
+    return out
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -234,6 +291,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-admm", action="store_true")
     ap.add_argument("--admm-iters", type=int, default=20)
+    ap.add_argument("--no-sweep", action="store_true", help="skip the C1 / C3 dimension sweep")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup) if args.impl == "ours" else args.warmup
 
@@ -380,6 +438,12 @@ def main():
     admm_line = None
     if not args.no_admm:
         admm_line = run_admm(args, rank, world, local, dev)
+    sweep = None
+    if rank == 0 and world == 1 and not args.no_sweep:
+        try:
+            sweep = run_sweep(args, dev)
+        except Exception as e:
+            sweep = [{"error": repr(e)}]
 
     traffic = None
     prof = os.path.join(ROOT, "profiles", "traffic.json")
@@ -410,6 +474,7 @@ def main():
             "parity": parity,
             "status_counts": {str(k): int(v) for k, v in zip(*np.unique(status, return_counts=True))},
             "admm": admm_line,
+            "sweep": sweep,
             "ms_per_step_all": ms_steps,
         }
         print(json.dumps(line), flush=True)

@@ -250,6 +250,18 @@ int check_batch(const tb_problem_batch* b, int64_t* nparams) {
 }
 
 constexpr int64_t kChunkMin = 4096;  // problems per chunk of the host-buffer pipeline
+
+// page-locked (or registered) host memory: async copies from pageable memory
+// block the host, which would serialise the chunk pipeline
+bool is_pinned(const void* p) {
+    if (!p) return true;
+    cudaPointerAttributes at;
+    if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return at.type == cudaMemoryTypeHost;
+}
 constexpr int64_t kMaxChunks = 8;
 
 struct OutPtrs {
@@ -384,7 +396,7 @@ extern "C" int tb_solve_batch(tb_context* ctx, const tb_problem_batch* b, const 
         }
     }
 
-    // Host buffers: the partition is cut into chunks, each on its own stream,
+    // Pinned host buffers: the partition is cut into chunks, each on its own stream,
     // so the H2D copy of chunk i+1 and the D2H copy of chunk i-1 overlap the
     // solves, and a long-running problem in one chunk never holds back the
     // next chunk (warp kernel; the persistent block kernel owns one workspace
@@ -394,7 +406,10 @@ extern "C" int tb_solve_batch(tb_context* ctx, const tb_problem_batch* b, const 
         CUDA_TRY(cudaSetDevice(d.device));
         const int64_t c = cnt[k];
         CUDA_TRY(cudaEventRecord(d.ev[0], d.stream));
-        const bool staged = (in_host || out_host) && c > 0;
+        const bool staged = (in_host || out_host) && c > 0 &&
+                            (!in_host || (is_pinned(b->x0) && is_pinned(b->lower) && is_pinned(b->upper) &&
+                                          (np == 0 || is_pinned(b->params)))) &&
+                            (!out_host || (is_pinned(r->x_star) && is_pinned(r->f_star) && is_pinned(r->status)));
         const int nch = (staged && n <= tbdev::max_warp_dim() && c >= 2 * kChunkMin)
                             ? (int)std::min<int64_t>(kMaxChunks, c / kChunkMin)
                             : 1;
