@@ -204,6 +204,26 @@ def run_admm(args, rank, world, local, dev):
             "config": {"workload": cfg, "n_bus": grid.n_bus, "n_branch": grid.n_branch, "n_gen": grid.n_gen,
                        "branch_dim": 4, "parallelism": f"branches sharded over {world} GPU(s), NCCL all-gather"},
             "residuals_first_last": [run.history[0], run.history[-1]]}
+    if world == 1:
+        # C4 with the line limits on: d=6 branch
+        # subproblems + the augmented-Lagrangian rounds inside every iteration
+        ll = A.AdmmSolver(grid, A.AdmmOptions(line_limits=True), local)
+        for _ in range(max(3, args.warmup)):
+            ll.step()
+        r0 = int(ll.get(A.AUGLAG_ROUNDS)[0])
+        k = max(5, args.admm_iters // 2)
+        torch.cuda.synchronize(dev)
+        t0 = time.perf_counter()
+        for _ in range(k):
+            ll.step()
+        torch.cuda.synchronize(dev)
+        dt = (time.perf_counter() - t0) / k
+        line["line_limits"] = {
+            "value": 1.0 / dt, "unit": "iter/s", "ms_per_iter": 1e3 * dt, "iters_timed": k,
+            "auglag_rounds_per_iter": (int(ll.get(A.AUGLAG_ROUNDS)[0]) - r0) / k,
+            "max_line_violation": float(ll.get(A.LINE_VIOL)[0]), "branch_dim": 6,
+            "timing": "host wall clock per blocking tb_admm_step (the AL loop reads the active count every round)"}
+        ll.close()
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
             from oracle import pyoracle

@@ -167,6 +167,8 @@ typedef struct tb_admm_grid {
     const double *gen_c2, *gen_c1, *gen_pmin, *gen_pmax, *gen_qmin, *gen_qmax;
     const int32_t *br_from, *br_to; /* [n_branch] */
     const double* br_coef;          /* [n_branch][8] pi-model flow coefficients (TB_BR_GFF..TB_BR_BTF) */
+    const double* br_smax2;         /* [n_branch] line limit s-bar^2 (per unit^2, Eq. (2c)); read only with
+                                       options.line_limits; NULL = unlimited */
 } tb_admm_grid;
 
 typedef struct tb_admm_options {
@@ -174,6 +176,20 @@ typedef struct tb_admm_options {
     double rho_va; /* voltage / angle couplings (4 rho0) */
     int32_t shard_rank, shard_count;
     tb_tron_config tron;
+    /* Line limits (SPEC.md:425 leaves Eq. (2c) out of
+     * Eq. (3)): 0 = the SPEC's d = 4 branch subproblem; 1 = the d = 6 variant
+     * with slacks s in [-s-bar^2, 0], h = p^2 + q^2 + s = 0 per line end,
+     * enforced by an augmented-Lagrangian loop around the branch TRON solves
+     * inside every ADMM iteration: solve the active branches, then per branch
+     * with hmax = max |h|: hmax <= feas_tol -> done; hmax <= eta -> mu += xi h,
+     * eta = max(feas_tol, 0.1 eta); else xi = min(xi_max, 10 xi).  mu carries
+     * over between ADMM iterations, xi and eta restart at xi0 / eta0. */
+    int32_t line_limits;
+    int32_t auglag_max_iter; /* AL rounds per ADMM iteration (default 20) */
+    double auglag_xi0;       /* default 10 */
+    double auglag_xi_max;    /* default 1e8 */
+    double auglag_eta0;      /* default 0.1 */
+    double auglag_feas_tol;  /* default 1e-6 */
 } tb_admm_options;
 
 typedef struct tb_admm tb_admm;
@@ -186,10 +202,12 @@ typedef struct tb_admm tb_admm;
 #define TB_ADMM_GEN_LQ 5
 #define TB_ADMM_BUS_WT 6
 #define TB_ADMM_BUS_TT 7
-#define TB_ADMM_BRANCH_X 8      /* [n_branch][4] (v_i, v_j, th_i, th_j) */
+#define TB_ADMM_BRANCH_X 8      /* [n_branch][dim] (v_i, v_j, th_i, th_j[, s_ij, s_ji]); dim 6 with line_limits */
 #define TB_ADMM_BRANCH_PARAMS 9 /* [n_branch][36] incl. lambda / rho / consensus */
 #define TB_ADMM_BRANCH_STATUS 10
 #define TB_ADMM_COST 11 /* sum_g c2 p^2 + c1 p */
+#define TB_ADMM_AUGLAG_ROUNDS 12 /* int64 [1]: AL rounds run so far (line_limits) */
+#define TB_ADMM_LINE_VIOL 13     /* double [1]: max over branches and ends of |h| (line_limits) */
 
 void tb_admm_options_default(tb_admm_options* opt);
 /* x_external: optional device buffer for the branch solutions,

@@ -6,7 +6,9 @@
  * consensus / multipliers / residuals — the closed forms are the shared
  * plain-C functions of csrc/tb_admm.h, evaluated sequentially in canonical
  * order.  Parity with the device is therefore exact (same bits per iteration);
- * the spec's own examples pin the closed forms (tests/test_admm.py).
+ * the spec's own examples pin the closed forms (tests/test_admm.py).  With
+ * line limits (options.line_limits) the branch stage is the augmented-
+ * Lagrangian loop of tb_admm_options, restated here in ascending order.
  */
 #include <stdlib.h>
 #include <string.h>
@@ -22,6 +24,10 @@ typedef struct orc_admm {
     int nb, ng, nl;
     double *pd, *qd, *gsh, *bsh, *c2, *c1, *pmin, *pmax, *qmin, *qmax, *xtmp;
     int32_t *gen_bus, *from, *to, *status;
+    int dim;                                /* 4, or 6 with line limits */
+    double *eta, *cx, *cl, *cu, *cp, *cxo;  /* augmented-Lagrangian state / compaction */
+    int32_t *active, *cidx, *cst;
+    long auglag_rounds;
 } orc_admm;
 
 static double* dup_d(const double* s, int n) {
@@ -59,13 +65,26 @@ int orc_admm_create(const tb_admm_grid* g, const tb_admm_options* o, int workers
     a->gen_bus = dup_i(g->gen_bus, a->ng);
     a->from = dup_i(g->br_from, a->nl);
     a->to = dup_i(g->br_to, a->nl);
-    a->xtmp = (double*)malloc(sizeof(double) * 4 * (size_t)a->nl);
+    a->dim = a->hs.dim;
+    a->xtmp = (double*)malloc(sizeof(double) * a->dim * (size_t)a->nl);
     a->status = (int32_t*)malloc(sizeof(int32_t) * (size_t)a->nl);
+    if (a->dim == 6) {
+        const size_t m = (size_t)(a->nl > 0 ? a->nl : 1);
+        a->eta = (double*)malloc(sizeof(double) * m);
+        a->cx = (double*)malloc(sizeof(double) * 6 * m);
+        a->cl = (double*)malloc(sizeof(double) * 6 * m);
+        a->cu = (double*)malloc(sizeof(double) * 6 * m);
+        a->cxo = (double*)malloc(sizeof(double) * 6 * m);
+        a->cp = (double*)malloc(sizeof(double) * TB_BR_NPARAMS * m);
+        a->active = (int32_t*)malloc(sizeof(int32_t) * m);
+        a->cidx = (int32_t*)malloc(sizeof(int32_t) * m);
+        a->cst = (int32_t*)malloc(sizeof(int32_t) * m);
+    }
     tb_admm_view* v = &a->v;
     v->n_bus = a->nb;
     v->n_gen = a->ng;
     v->n_branch = a->nl;
-    v->branch_dim = 4;
+    v->branch_dim = a->dim;
     v->bus_pd = a->pd;
     v->bus_qd = a->qd;
     v->bus_gsh = a->gsh;
@@ -99,13 +118,61 @@ int orc_admm_create(const tb_admm_grid* g, const tb_admm_options* o, int workers
     return 0;
 }
 
+/* Branch stage for rows [lo, hi): one warm-started batched TRON solve (d = 4),
+ * or the augmented-Lagrangian rounds of the line-limit variant (d = 6, see
+ * tb_admm_options in include/tb_capi.h): solve the active branches (compacted
+ * in ascending order), then tb_admm_auglag_update per solved branch. */
+static int orc_branch_stage(orc_admm* a, int64_t lo, int64_t hi) {
+    const int D = a->dim;
+    if (hi <= lo) return 0;
+    const int64_t cnt = hi - lo;
+    if (D == 4) {
+        const int rc = orc_solve_batch(TB_FAMILY_BRANCH, 4, cnt, a->hs.br_x + lo * 4, a->hs.br_lower + lo * 4,
+                                       a->hs.br_upper + lo * 4, a->hs.br_params + lo * TB_BR_NPARAMS,
+                                       TB_BR_NPARAMS, &a->opt.tron, a->workers, a->xtmp, NULL, NULL, a->status + lo,
+                                       NULL, NULL, NULL, NULL, NULL, NULL, NULL);
+        memcpy(a->hs.br_x + lo * 4, a->xtmp, sizeof(double) * 4 * (size_t)cnt);
+        return rc;
+    }
+    for (int64_t l = lo; l < hi; ++l) {
+        a->hs.br_params[l * TB_BR_NPARAMS + TB_BR_XI] = a->opt.auglag_xi0;
+        a->eta[l] = a->opt.auglag_eta0;
+        a->active[l] = 1;
+    }
+    int rc = 0;
+    for (int round = 0; round < a->opt.auglag_max_iter; ++round) {
+        int64_t m = 0;
+        for (int64_t l = lo; l < hi; ++l) {
+            if (!a->active[l]) continue;
+            a->cidx[m] = (int32_t)l;
+            memcpy(a->cx + m * 6, a->hs.br_x + l * 6, sizeof(double) * 6);
+            memcpy(a->cl + m * 6, a->hs.br_lower + l * 6, sizeof(double) * 6);
+            memcpy(a->cu + m * 6, a->hs.br_upper + l * 6, sizeof(double) * 6);
+            memcpy(a->cp + m * TB_BR_NPARAMS, a->hs.br_params + l * TB_BR_NPARAMS, sizeof(double) * TB_BR_NPARAMS);
+            ++m;
+        }
+        if (m == 0) break;
+        ++a->auglag_rounds;
+        const int r = orc_solve_batch(TB_FAMILY_BRANCH, 6, m, a->cx, a->cl, a->cu, a->cp, TB_BR_NPARAMS,
+                                      &a->opt.tron, a->workers, a->cxo, NULL, NULL, a->cst, NULL, NULL, NULL, NULL,
+                                      NULL, NULL, NULL);
+        if (r && !rc) rc = r;
+        for (int64_t k = 0; k < m; ++k) {
+            const int64_t l = a->cidx[k];
+            double* x = a->hs.br_x + l * 6;
+            memcpy(x, a->cxo + k * 6, sizeof(double) * 6);
+            a->status[l] = a->cst[k];
+            a->active[l] = tb_admm_auglag_update(x, a->hs.br_params + l * TB_BR_NPARAMS, a->eta + l,
+                                                 a->opt.auglag_feas_tol, a->opt.auglag_xi_max);
+        }
+    }
+    return rc;
+}
+
 /* One iteration. Returns 0 or the TRON error status. */
 int orc_admm_step(orc_admm* a, double* primal, double* dual) {
     for (int g = 0; g < a->ng; ++g) tb_admm_gen_update(&a->v, g);
-    const int rc = orc_solve_batch(TB_FAMILY_BRANCH, 4, a->nl, a->hs.br_x, a->hs.br_lower, a->hs.br_upper,
-                                   a->hs.br_params, TB_BR_NPARAMS, &a->opt.tron, a->workers, a->xtmp, NULL, NULL,
-                                   a->status, NULL, NULL, NULL, NULL, NULL, NULL, NULL);
-    memcpy(a->hs.br_x, a->xtmp, sizeof(double) * 4 * (size_t)a->nl);
+    const int rc = orc_branch_stage(a, 0, a->nl);
     double pr = 0.0, du = 0.0;
     for (int b = 0; b < a->nb; ++b) {
         tb_admm_res r;
@@ -130,7 +197,19 @@ int orc_admm_get(orc_admm* a, int what, void* out) {
         case TB_ADMM_GEN_LQ: src = a->hs.gen_lq; bytes = sizeof(double) * a->ng; break;
         case TB_ADMM_BUS_WT: src = a->hs.bus_wt; bytes = sizeof(double) * a->nb; break;
         case TB_ADMM_BUS_TT: src = a->hs.bus_tt; bytes = sizeof(double) * a->nb; break;
-        case TB_ADMM_BRANCH_X: src = a->hs.br_x; bytes = sizeof(double) * 4 * (size_t)a->nl; break;
+        case TB_ADMM_BRANCH_X: src = a->hs.br_x; bytes = sizeof(double) * a->dim * (size_t)a->nl; break;
+        case TB_ADMM_AUGLAG_ROUNDS: *(int64_t*)out = a->auglag_rounds; return 0;
+        case TB_ADMM_LINE_VIOL: {
+            if (a->dim != 6) return 1;
+            double m = 0.0, h[2];
+            for (int l = 0; l < a->nl; ++l) {
+                double v = tb_admm_line_hmax(a->hs.br_x + (long)l * 6, a->hs.br_params + (long)l * TB_BR_NPARAMS, h);
+                if (!(v >= 0.0)) v = 1.0 / 0.0;
+                if (m < v) m = v;
+            }
+            *(double*)out = m;
+            return 0;
+        }
         case TB_ADMM_BRANCH_PARAMS: src = a->hs.br_params; bytes = sizeof(double) * TB_BR_NPARAMS * (size_t)a->nl; break;
         case TB_ADMM_BRANCH_STATUS: src = a->status; bytes = sizeof(int32_t) * (size_t)a->nl; break;
         case TB_ADMM_COST: {
@@ -149,7 +228,8 @@ void orc_admm_destroy(orc_admm* a) {
     if (!a) return;
     tb_admm_host_free(&a->hs);
     void* ps[] = {a->pd, a->qd, a->gsh, a->bsh, a->c2, a->c1, a->pmin, a->pmax, a->qmin, a->qmax,
-                  a->xtmp, a->gen_bus, a->from, a->to, a->status};
+                  a->xtmp, a->gen_bus, a->from, a->to, a->status, a->eta, a->cx, a->cl, a->cu, a->cp, a->cxo,
+                  a->active, a->cidx, a->cst};
     for (size_t k = 0; k < sizeof ps / sizeof ps[0]; ++k) free(ps[k]);
     free(a);
 }
@@ -171,14 +251,7 @@ double orc_admm_gen_p(double c2, double c1, double lam, double rho, double ptil,
 /* generator update (all) + branch TRON for rows [lo, hi) in place */
 int orc_admm_solve_components(orc_admm* a, int64_t lo, int64_t hi) {
     for (int g = 0; g < a->ng; ++g) tb_admm_gen_update(&a->v, g);
-    if (hi <= lo) return 0;
-    const int64_t cnt = hi - lo;
-    const int rc = orc_solve_batch(TB_FAMILY_BRANCH, 4, cnt, a->hs.br_x + lo * 4, a->hs.br_lower + lo * 4,
-                                   a->hs.br_upper + lo * 4, a->hs.br_params + lo * TB_BR_NPARAMS, TB_BR_NPARAMS,
-                                   &a->opt.tron, a->workers, a->xtmp, NULL, NULL, a->status + lo, NULL, NULL, NULL,
-                                   NULL, NULL, NULL, NULL);
-    memcpy(a->hs.br_x + lo * 4, a->xtmp, sizeof(double) * 4 * (size_t)cnt);
-    return rc;
+    return orc_branch_stage(a, lo, hi);
 }
 double* orc_admm_x(orc_admm* a) { return a->hs.br_x; }
 /* bus update over every bus; residual maxima over buses [blo, bhi) */

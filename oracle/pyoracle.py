@@ -178,7 +178,9 @@ class OracleAdmm:
         self.lib = oracle_lib().lib
         self.grid = grid
         g, self._keep = grid.to_c()
-        o = (options or AdmmOptions()).to_c(0, 1)
+        options = options or AdmmOptions()
+        self.dim = options.branch_dim
+        o = options.to_c(0, 1)
         h = C.c_void_p()
         self.lib.orc_admm_create.argtypes = [C.c_void_p, C.c_void_p, C.c_int, C.POINTER(C.c_void_p)]
         assert self.lib.orc_admm_create(C.addressof(g), C.addressof(o), int(workers), C.byref(h)) == 0
@@ -198,9 +200,10 @@ class OracleAdmm:
         from paper_2106_14995_b200 import admm as A
 
         g = self.grid
-        shapes = {A.BRANCH_X: ((g.n_branch, 4), np.float64), A.BRANCH_PARAMS: ((g.n_branch, 36), np.float64),
+        shapes = {A.BRANCH_X: ((g.n_branch, self.dim), np.float64), A.BRANCH_PARAMS: ((g.n_branch, 36), np.float64),
                   A.BRANCH_STATUS: ((g.n_branch,), np.int32), A.BUS_WT: ((g.n_bus,), np.float64),
-                  A.BUS_TT: ((g.n_bus,), np.float64), A.COST: ((1,), np.float64)}
+                  A.BUS_TT: ((g.n_bus,), np.float64), A.COST: ((1,), np.float64),
+                  A.AUGLAG_ROUNDS: ((1,), np.int64), A.LINE_VIOL: ((1,), np.float64)}
         shape, dt = shapes.get(what, ((g.n_gen,), np.float64))
         out = np.zeros(shape, dt)
         self.lib.orc_admm_get.argtypes = [C.c_void_p, C.c_int, C.c_void_p]

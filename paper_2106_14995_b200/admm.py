@@ -21,6 +21,7 @@ from .tron import SolverError, TronConfig
 
 GEN_P, GEN_Q, GEN_PT, GEN_QT, GEN_LP, GEN_LQ, BUS_WT, BUS_TT = range(8)
 BRANCH_X, BRANCH_PARAMS, BRANCH_STATUS, COST = 8, 9, 10, 11
+AUGLAG_ROUNDS, LINE_VIOL = 12, 13
 
 
 @dataclass
@@ -43,6 +44,7 @@ class Grid:
     br_from: np.ndarray
     br_to: np.ndarray
     br_coef: np.ndarray  # [n_branch, 8]
+    br_smax2: Optional[np.ndarray] = None  # [n_branch] line limit s-bar^2 (per unit^2); None = unlimited
 
     @property
     def n_bus(self):
@@ -63,6 +65,9 @@ class Grid:
         g.n_bus, g.n_gen, g.n_branch = self.n_bus, self.n_gen, self.n_branch
         for name, _ in GridC._fields_[3:]:
             a = getattr(self, name)
+            if a is None:  # optional arrays (br_smax2)
+                setattr(g, name, None)
+                continue
             a = np.ascontiguousarray(a, dtype=np.int32 if name in ("gen_bus", "br_from", "br_to") else np.float64)
             keep[name] = a
             setattr(g, name, a.ctypes.data)
@@ -73,12 +78,14 @@ class GridC(C.Structure):
     _fields_ = [("n_bus", C.c_int32), ("n_gen", C.c_int32), ("n_branch", C.c_int32)] + [
         (n, C.c_void_p) for n in ("bus_pd", "bus_qd", "bus_gsh", "bus_bsh", "bus_vmin", "bus_vmax", "gen_bus",
                                   "gen_c2", "gen_c1", "gen_pmin", "gen_pmax", "gen_qmin", "gen_qmax", "br_from",
-                                  "br_to", "br_coef")]
+                                  "br_to", "br_coef", "br_smax2")]
 
 
 class OptionsC(C.Structure):
     _fields_ = [("rho_pq", C.c_double), ("rho_va", C.c_double), ("shard_rank", C.c_int32),
-                ("shard_count", C.c_int32), ("tron", L.TronConfigC)]
+                ("shard_count", C.c_int32), ("tron", L.TronConfigC), ("line_limits", C.c_int32),
+                ("auglag_max_iter", C.c_int32), ("auglag_xi0", C.c_double), ("auglag_xi_max", C.c_double),
+                ("auglag_eta0", C.c_double), ("auglag_feas_tol", C.c_double)]
 
 
 @dataclass
@@ -86,11 +93,27 @@ class AdmmOptions:
     rho_pq: float = 10.0  # SPEC.md:426 rho0
     rho_va: float = 40.0  # 4 rho0
     tron: TronConfig = field(default_factory=TronConfig)
+    # line limits (tb_admm_options): d = 6 branch subproblems + an augmented-
+    # Lagrangian loop per ADMM iteration
+    line_limits: bool = False
+    auglag_max_iter: int = 20
+    auglag_xi0: float = 10.0
+    auglag_xi_max: float = 1e8
+    auglag_eta0: float = 0.1
+    auglag_feas_tol: float = 1e-6
+
+    @property
+    def branch_dim(self) -> int:
+        return 6 if self.line_limits else 4
 
     def to_c(self, rank=0, world=1) -> OptionsC:
         o = OptionsC()
         o.rho_pq, o.rho_va, o.shard_rank, o.shard_count = self.rho_pq, self.rho_va, rank, world
         o.tron = self.tron.to_c()
+        o.line_limits = 1 if self.line_limits else 0
+        o.auglag_max_iter = self.auglag_max_iter
+        o.auglag_xi0, o.auglag_xi_max = self.auglag_xi0, self.auglag_xi_max
+        o.auglag_eta0, o.auglag_feas_tol = self.auglag_eta0, self.auglag_feas_tol
         return o
 
 
@@ -175,10 +198,12 @@ class AdmmSolver:
 
     def get(self, what: int) -> np.ndarray:
         g = self.grid
-        if what == COST:
+        if what in (COST, LINE_VIOL):
             out = np.zeros(1)
+        elif what == AUGLAG_ROUNDS:
+            out = np.zeros(1, np.int64)
         elif what in (BRANCH_X,):
-            out = np.zeros((g.n_branch, 4))
+            out = np.zeros((g.n_branch, self.options.branch_dim))
         elif what == BRANCH_PARAMS:
             out = np.zeros((g.n_branch, 36))
         elif what == BRANCH_STATUS:
@@ -201,8 +226,9 @@ class ShardedAdmm:
         self.dev = torch.device("cuda", device)
         chunk = (grid.n_branch + world - 1) // world
         self.chunk, self.rank, self.world = chunk, rank, world
+        dim = (options or AdmmOptions()).branch_dim
         # the branch-solution buffer the all-gather writes into (caller-owned)
-        self.x = torch.zeros((chunk * world, 4), dtype=torch.float64, device=self.dev)
+        self.x = torch.zeros((chunk * world, dim), dtype=torch.float64, device=self.dev)
         self.res = torch.zeros(2, dtype=torch.float64, device=self.dev)
         self.solver = AdmmSolver(grid, options, device, rank, world, x_buffer_ptr=self.x.data_ptr())
         self.history: List[Tuple[float, float]] = []

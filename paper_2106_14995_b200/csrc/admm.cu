@@ -11,6 +11,7 @@
 //                          buses -> the caller max-allreduces two doubles)
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cmath>
 #include <cstring>
 #include <string>
@@ -60,6 +61,55 @@ __global__ void admm_cost_kernel(tb_admm_view v, double* out) {
     }
 }
 
+// ---- line limits: augmented-Lagrangian rounds over this shard's branches
+__global__ void admm_auglag_reset_kernel(double* prm, double* eta, int32_t* active, int64_t lo, int64_t hi,
+                                         double xi0, double eta0) {
+    const int64_t l = lo + blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (l >= hi) return;
+    prm[l * TB_BR_NPARAMS + TB_BR_XI] = xi0;
+    eta[l] = eta0;
+    active[l] = 1;
+}
+
+// compact the active branches of [lo, hi) into a dense TRON batch (slot order
+// is arbitrary: every problem's result is independent of its position)
+__global__ void admm_auglag_gather_kernel(const int32_t* active, int64_t lo, int64_t hi, const double* x,
+                                          const double* xl, const double* xu, const double* prm, int32_t* cnt,
+                                          int32_t* idx, double* cx, double* cl, double* cu, double* cp) {
+    const int64_t l = lo + blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (l >= hi || !active[l]) return;
+    const int k = atomicAdd(cnt, 1);
+    idx[k] = (int32_t)l;
+    for (int i = 0; i < 6; ++i) {
+        cx[k * 6 + i] = x[l * 6 + i];
+        cl[k * 6 + i] = xl[l * 6 + i];
+        cu[k * 6 + i] = xu[l * 6 + i];
+    }
+    for (int i = 0; i < TB_BR_NPARAMS; ++i) cp[k * TB_BR_NPARAMS + i] = prm[l * TB_BR_NPARAMS + i];
+}
+
+// scatter the solutions back and run the AL update of each solved branch
+__global__ void admm_auglag_update_kernel(const int32_t* cnt, const int32_t* idx, const double* cx,
+                                          const int32_t* cst, double* x, int32_t* status, double* prm, double* eta,
+                                          int32_t* active, double feas_tol, double xi_max) {
+    const int k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= *cnt) return;
+    const int64_t l = idx[k];
+    double* xl = x + l * 6;
+    for (int i = 0; i < 6; ++i) xl[i] = cx[k * 6 + i];
+    status[l] = cst[k];
+    active[l] = tb_admm_auglag_update(xl, prm + l * TB_BR_NPARAMS, eta + l, feas_tol, xi_max);
+}
+
+__global__ void admm_line_viol_kernel(const double* x, const double* prm, int64_t n, unsigned long long* out) {
+    const int64_t l = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    double h[2];
+    double v = l < n ? tb_admm_line_hmax(x + l * 6, prm + l * TB_BR_NPARAMS, h) : 0.0;
+    if (!(v >= 0.0)) v = CUDART_INF;
+    v = tbdev::warp_max_nonneg(v);
+    if ((threadIdx.x & 31) == 0) atomicMax(out, (unsigned long long)__double_as_longlong(v));
+}
+
 thread_local std::string g_admm_err;
 
 int fail(int code, const std::string& m) {
@@ -84,6 +134,16 @@ struct tb_admm {
     int bus_lo = 0, bus_hi = 0;
     tb_tron_config tron{};
     long long iterations = 0;
+    // line limits (dim 6)
+    int dim = 4;
+    tb_admm_options opt{};
+    double* eta = nullptr;
+    int32_t* active = nullptr;
+    int32_t* cnt = nullptr;
+    int32_t* cidx = nullptr;
+    double *cx = nullptr, *cl = nullptr, *cu = nullptr, *cp = nullptr, *cxo = nullptr;
+    int32_t* cst = nullptr;
+    long long auglag_rounds = 0;
 };
 
 namespace {
@@ -115,6 +175,12 @@ void tb_admm_options_default(tb_admm_options* o) {
     o->shard_rank = 0;
     o->shard_count = 1;
     tb_config_default(&o->tron);
+    o->line_limits = 0;
+    o->auglag_max_iter = 20;
+    o->auglag_xi0 = 10.0;
+    o->auglag_xi_max = 1e8;
+    o->auglag_eta0 = 0.1;
+    o->auglag_feas_tol = 1e-6;
 }
 
 int tb_admm_create(const tb_admm_grid* gr, const tb_admm_options* opt, int32_t device, double* x_external,
@@ -127,6 +193,10 @@ int tb_admm_create(const tb_admm_grid* gr, const tb_admm_options* opt, int32_t d
         return fail(TB_E_INVALID_ARGUMENT, "tb_admm_create: bad shard");
     if (!(opt->rho_pq > 0.0) || !(opt->rho_va > 0.0)) return fail(TB_E_INVALID_ARGUMENT, "tb_admm_create: rho must be > 0");
     if (tb_config_validate(&opt->tron) != TB_OK) return fail(TB_E_INVALID_ARGUMENT, tb_last_error());
+    if (opt->line_limits &&
+        (opt->auglag_max_iter < 1 || !(opt->auglag_xi0 > 0.0) || !(opt->auglag_xi_max >= opt->auglag_xi0) ||
+         !(opt->auglag_eta0 > 0.0) || !(opt->auglag_feas_tol > 0.0)))
+        return fail(TB_E_INVALID_ARGUMENT, "tb_admm_create: bad augmented-Lagrangian options");
     const int nb = gr->n_bus, ng = gr->n_gen, nl = gr->n_branch;
     for (int l = 0; l < nl; ++l)
         if (gr->br_from[l] < 0 || gr->br_from[l] >= nb || gr->br_to[l] < 0 || gr->br_to[l] >= nb)
@@ -147,6 +217,9 @@ int tb_admm_create(const tb_admm_grid* gr, const tb_admm_options* opt, int32_t d
     tb_admm* a = new tb_admm;
     a->device = device;
     a->tron = opt->tron;
+    a->opt = *opt;
+    const int D = hs.dim;
+    a->dim = D;
     int prev = 0;
     cudaGetDevice(&prev);
     cudaError_t err = cudaSetDevice(device);
@@ -166,7 +239,7 @@ int tb_admm_create(const tb_admm_grid* gr, const tb_admm_options* opt, int32_t d
     v.n_bus = nb;
     v.n_gen = ng;
     v.n_branch = nl;
-    v.branch_dim = 4;
+    v.branch_dim = D;
 #define ALLOC_UP(field, T, n, src)                                       \
     do {                                                                 \
         T* p_ = dalloc<T>(a, (n), &err);                                 \
@@ -206,17 +279,30 @@ int tb_admm_create(const tb_admm_grid* gr, const tb_admm_options* opt, int32_t d
 #undef ALLOC_UP
     if (err == cudaSuccess) {
         if (x_external) a->x = x_external;
-        else a->x = dalloc<double>(a, (size_t)rows * 4, &err);
+        else a->x = dalloc<double>(a, (size_t)rows * D, &err);
     }
-    if (err == cudaSuccess) err = upload<double>(a->x, hs.br_x, (size_t)nl * 4);
+    if (err == cudaSuccess) err = upload<double>(a->x, hs.br_x, (size_t)nl * D);
     if (err == cudaSuccess) {
-        a->lower = dalloc<double>(a, (size_t)nl * 4, &err);
-        if (err == cudaSuccess) err = upload<double>(a->lower, hs.br_lower, (size_t)nl * 4);
-        a->upper = dalloc<double>(a, (size_t)nl * 4, &err);
-        if (err == cudaSuccess) err = upload<double>(a->upper, hs.br_upper, (size_t)nl * 4);
+        a->lower = dalloc<double>(a, (size_t)nl * D, &err);
+        if (err == cudaSuccess) err = upload<double>(a->lower, hs.br_lower, (size_t)nl * D);
+        a->upper = dalloc<double>(a, (size_t)nl * D, &err);
+        if (err == cudaSuccess) err = upload<double>(a->upper, hs.br_upper, (size_t)nl * D);
         a->status = dalloc<int32_t>(a, (size_t)nl, &err);
         a->res = dalloc<unsigned long long>(a, 2, &err);
         a->cost = dalloc<double>(a, 1, &err);
+    }
+    if (err == cudaSuccess && D == 6) {  // AL state + compaction buffers for this shard
+        const size_t m = (size_t)std::max<int64_t>(1, a->br_hi - a->br_lo);
+        a->eta = dalloc<double>(a, (size_t)nl, &err);
+        a->active = dalloc<int32_t>(a, (size_t)nl, &err);
+        a->cnt = dalloc<int32_t>(a, 1, &err);
+        a->cidx = dalloc<int32_t>(a, m, &err);
+        a->cx = dalloc<double>(a, m * 6, &err);
+        a->cl = dalloc<double>(a, m * 6, &err);
+        a->cu = dalloc<double>(a, m * 6, &err);
+        a->cxo = dalloc<double>(a, m * 6, &err);
+        a->cp = dalloc<double>(a, m * TB_BR_NPARAMS, &err);
+        a->cst = dalloc<int32_t>(a, m, &err);
     }
     v.br_x = a->x;
     tb_admm_host_free(&hs);
@@ -256,7 +342,34 @@ int tb_admm_solve_components(tb_admm* a, void* stream) {
     cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : a->stream;
     if (a->v.n_gen > 0) admm_gen_kernel<<<(a->v.n_gen + 127) / 128, 128, 0, st>>>(a->v);
     const int64_t cnt = a->br_hi - a->br_lo;
-    if (cnt > 0) {
+    if (cnt > 0 && a->dim == 6) {
+        // augmented-Lagrangian rounds: solve the active branches, update mu / xi
+        const unsigned gb = (unsigned)((cnt + 127) / 128);
+        admm_auglag_reset_kernel<<<gb, 128, 0, st>>>(a->v.br_params, a->eta, a->active, a->br_lo, a->br_hi,
+                                                     a->opt.auglag_xi0, a->opt.auglag_eta0);
+        for (int round = 0; round < a->opt.auglag_max_iter; ++round) {
+            cudaMemsetAsync(a->cnt, 0, sizeof(int32_t), st);
+            admm_auglag_gather_kernel<<<gb, 128, 0, st>>>(a->active, a->br_lo, a->br_hi, a->x, a->lower, a->upper,
+                                                          a->v.br_params, a->cnt, a->cidx, a->cx, a->cl, a->cu,
+                                                          a->cp);
+            int32_t nact = 0;
+            cudaMemcpyAsync(&nact, a->cnt, sizeof nact, cudaMemcpyDeviceToHost, st);
+            const cudaError_t e = cudaStreamSynchronize(st);
+            if (e != cudaSuccess) return fail(TB_E_CUDA, cudaGetErrorString(e));
+            if (nact == 0) break;
+            ++a->auglag_rounds;
+            tb_problem_batch b{TB_FAMILY_BRANCH, 6, nact, a->cx, a->cl, a->cu, a->cp, TB_BR_NPARAMS, TB_MEM_DEVICE};
+            tb_batch_result r{};
+            r.x_star = a->cxo;
+            r.status = a->cst;
+            r.memspace = TB_MEM_DEVICE;
+            const int rc = tb_solve_batch_async(a->ctx, &b, &a->tron, &r, st);
+            if (rc != TB_OK) return fail(rc, tb_last_error());
+            admm_auglag_update_kernel<<<(unsigned)((nact + 127) / 128), 128, 0, st>>>(
+                a->cnt, a->cidx, a->cxo, a->cst, a->x, a->status, a->v.br_params, a->eta, a->active,
+                a->opt.auglag_feas_tol, a->opt.auglag_xi_max);
+        }
+    } else if (cnt > 0) {
         tb_problem_batch b{TB_FAMILY_BRANCH, 4, cnt, a->x + a->br_lo * 4, a->lower + a->br_lo * 4,
                            a->upper + a->br_lo * 4, a->v.br_params + a->br_lo * TB_BR_NPARAMS, TB_BR_NPARAMS,
                            TB_MEM_DEVICE};
@@ -329,7 +442,22 @@ int tb_admm_get(tb_admm* a, int32_t what, void* host_out) {
         case TB_ADMM_GEN_LQ: src = v.gen_lq; bytes = sizeof(double) * v.n_gen; break;
         case TB_ADMM_BUS_WT: src = v.bus_wt; bytes = sizeof(double) * v.n_bus; break;
         case TB_ADMM_BUS_TT: src = v.bus_tt; bytes = sizeof(double) * v.n_bus; break;
-        case TB_ADMM_BRANCH_X: src = a->x; bytes = sizeof(double) * 4 * (size_t)v.n_branch; break;
+        case TB_ADMM_BRANCH_X: src = a->x; bytes = sizeof(double) * a->dim * (size_t)v.n_branch; break;
+        case TB_ADMM_AUGLAG_ROUNDS: {
+            const int64_t r = a->auglag_rounds;
+            std::memcpy(host_out, &r, sizeof r);
+            return TB_OK;
+        }
+        case TB_ADMM_LINE_VIOL: {
+            if (a->dim != 6) return fail(TB_E_INVALID_ARGUMENT, "tb_admm_get: line limits are off");
+            unsigned long long* m = reinterpret_cast<unsigned long long*>(a->cost);
+            cudaMemsetAsync(m, 0, sizeof *m, a->stream);
+            admm_line_viol_kernel<<<(unsigned)((v.n_branch + 127) / 128), 128, 0, a->stream>>>(a->x, v.br_params,
+                                                                                               v.n_branch, m);
+            src = a->cost;
+            bytes = sizeof(double);
+            break;
+        }
         case TB_ADMM_BRANCH_PARAMS: src = v.br_params; bytes = sizeof(double) * TB_BR_NPARAMS * (size_t)v.n_branch; break;
         case TB_ADMM_BRANCH_STATUS: src = a->status; bytes = sizeof(int32_t) * (size_t)v.n_branch; break;
         case TB_ADMM_COST: {
@@ -340,7 +468,8 @@ int tb_admm_get(tb_admm* a, int32_t what, void* host_out) {
         }
         default: return fail(TB_E_INVALID_ARGUMENT, "tb_admm_get: unknown field");
     }
-    const cudaError_t e = cudaMemcpy(host_out, src, bytes, cudaMemcpyDeviceToHost);
+    cudaError_t e = cudaStreamSynchronize(a->stream);  // the COST / LINE_VIOL kernels ran on a->stream
+    if (e == cudaSuccess) e = cudaMemcpy(host_out, src, bytes, cudaMemcpyDeviceToHost);
     return e == cudaSuccess ? TB_OK : fail(TB_E_CUDA, cudaGetErrorString(e));
 }
 

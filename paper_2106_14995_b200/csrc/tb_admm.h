@@ -181,6 +181,40 @@ TB_HD void tb_admm_bus_update(const tb_admm_view* v, int b, tb_admm_res* res) {
     res->dual = du;
 }
 
+/* ---- line limits (options.line_limits, branch dim 6) ------------------
+ * h_l = p_l^2 + q_l^2 + s_l at the branch solution x, line end l (0 = from,
+ * 1 = to), with the BRANCH family's own flow expressions (tb_br_line). */
+TB_HD double tb_admm_line_hmax(const double* x, const double* prm, double* h) {
+    double base[8];
+    tb_br_base(x, base);
+    double hmax = 0.0;
+    for (int l = 0; l < 2; ++l) {
+        const double p = tb_admm_flow(base, prm, 2 * l), q = tb_admm_flow(base, prm, 2 * l + 1);
+        h[l] = (p * p + q * q) + x[4 + l];
+        const double a = tb_admm_absd(h[l]);
+        if (!(a <= hmax)) hmax = a; /* NaN propagates */
+    }
+    return hmax;
+}
+
+/* One augmented-Lagrangian round of one branch after its TRON solve (see
+ * tb_admm_options): updates mu / xi in the branch's parameter row and its eta;
+ * returns 1 while the branch stays active. */
+TB_HD int tb_admm_auglag_update(const double* x, double* prm, double* eta, double feas_tol, double xi_max) {
+    double h[2];
+    const double hmax = tb_admm_line_hmax(x, prm, h);
+    if (hmax <= *eta) {
+        if (hmax <= feas_tol) return 0;
+        const double xi = prm[TB_BR_XI];
+        prm[TB_BR_MU] += xi * h[0];
+        prm[TB_BR_MU + 1] += xi * h[1];
+        *eta = tb_smax(feas_tol, 0.1 * *eta);
+    } else {
+        prm[TB_BR_XI] = tb_smin(xi_max, 10.0 * prm[TB_BR_XI]);
+    }
+    return 1;
+}
+
 /* sum_g c2 p^2 + c1 p (generation cost at the component copies) */
 TB_HD double tb_admm_gen_cost(const tb_admm_view* v, int g) {
     const double p = v->gen_p[g];

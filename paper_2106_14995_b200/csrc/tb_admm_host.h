@@ -9,6 +9,7 @@
 #ifndef TB_ADMM_HOST_H
 #define TB_ADMM_HOST_H
 
+#include <stdio.h>
 #include <stdlib.h>
 #include <string.h>
 
@@ -20,6 +21,7 @@ typedef struct {
     double *gen_p, *gen_q, *gen_lp, *gen_lq, *gen_rp, *gen_rq, *gen_pt, *gen_qt;
     double *br_params, *br_x, *br_lower, *br_upper;
     int32_t *gen_ptr, *gen_idx, *end_ptr, *end_idx;
+    int dim; /* branch dimension: 4, or 6 with line limits */
     char err[256];
 } tb_admm_host_state;
 
@@ -35,6 +37,8 @@ static inline int tb_admm_host_init(const tb_admm_grid* g, const tb_admm_options
     const int nb = g->n_bus, ng = g->n_gen, nl = g->n_branch;
     const double two_pi = 2.0 * 3.14159265358979323846;
     memset(s, 0, sizeof(*s));
+    const int D = o->line_limits ? 6 : 4;
+    s->dim = D;
 #define TB_A(p, T, n) (p) = (T*)calloc((size_t)((n) > 0 ? (n) : 1), sizeof(T))
     TB_A(s->bus_wt, double, nb);
     TB_A(s->bus_tt, double, nb);
@@ -47,9 +51,9 @@ static inline int tb_admm_host_init(const tb_admm_grid* g, const tb_admm_options
     TB_A(s->gen_pt, double, ng);
     TB_A(s->gen_qt, double, ng);
     TB_A(s->br_params, double, (long)nl * TB_BR_NPARAMS);
-    TB_A(s->br_x, double, (long)nl * 4);
-    TB_A(s->br_lower, double, (long)nl * 4);
-    TB_A(s->br_upper, double, (long)nl * 4);
+    TB_A(s->br_x, double, (long)nl * D);
+    TB_A(s->br_lower, double, (long)nl * D);
+    TB_A(s->br_upper, double, (long)nl * D);
     TB_A(s->gen_ptr, int32_t, nb + 1);
     TB_A(s->gen_idx, int32_t, ng);
     TB_A(s->end_ptr, int32_t, nb + 1);
@@ -86,7 +90,7 @@ static inline int tb_admm_host_init(const tb_admm_grid* g, const tb_admm_options
     }
     for (int l = 0; l < nl; ++l) {
         double* prm = s->br_params + (long)l * TB_BR_NPARAMS;
-        double* x = s->br_x + (long)l * 4;
+        double* x = s->br_x + (long)l * D;
         for (int k = 0; k < 8; ++k) prm[k] = g->br_coef[(long)l * 8 + k];
         x[0] = 1.0;
         x[1] = 1.0;
@@ -108,8 +112,8 @@ static inline int tb_admm_host_init(const tb_admm_grid* g, const tb_admm_options
             prm[TB_BR_TTIL + e] = 0.0;
         }
         const int fb = g->br_from[l], tb = g->br_to[l];
-        double* lo = s->br_lower + (long)l * 4;
-        double* up = s->br_upper + (long)l * 4;
+        double* lo = s->br_lower + (long)l * D;
+        double* up = s->br_upper + (long)l * D;
         lo[0] = g->bus_vmin[fb];
         lo[1] = g->bus_vmin[tb];
         lo[2] = -two_pi;
@@ -118,6 +122,22 @@ static inline int tb_admm_host_init(const tb_admm_grid* g, const tb_admm_options
         up[1] = g->bus_vmax[tb];
         up[2] = two_pi;
         up[3] = two_pi;
+        if (D == 6) { /* slacks s in [-s-bar^2, 0], started at the flat-start flows */
+            const double sm2 = g->br_smax2 ? g->br_smax2[l] : HUGE_VAL;
+            if (!(sm2 >= 0.0)) {
+                snprintf(s->err, sizeof s->err, "tb_admm_create: branch %d line limit s-bar^2 must be >= 0", l);
+                return 1;
+            }
+            prm[TB_BR_MU] = prm[TB_BR_MU + 1] = 0.0;
+            prm[TB_BR_XI] = o->auglag_xi0;
+            prm[TB_BR_SMAX2] = sm2;
+            for (int e = 0; e < 2; ++e) {
+                const double p = tb_admm_flow(base, prm, 2 * e), q = tb_admm_flow(base, prm, 2 * e + 1);
+                lo[4 + e] = -sm2;
+                up[4 + e] = 0.0;
+                x[4 + e] = tb_smax(-(p * p + q * q), -sm2);
+            }
+        }
     }
     return 0;
 }

@@ -179,7 +179,8 @@ def make(family: str, count: int, dim: int, seed: int = None) -> ProblemBatch:
 
 
 # ------------------------------------------------------------------ ADMM grids
-def grid(n_bus: int, n_branch: int, n_gen: int, seed: int = 4, load_factor: float = 0.6, shunt_frac: float = 0.1):
+def grid(n_bus: int, n_branch: int, n_gen: int, seed: int = 4, load_factor: float = 0.6, shunt_frac: float = 0.1,
+         rate: tuple = (0.5, 3.0)):
     """Synthetic AC-OPF network: random spanning tree plus
     extra edges up to n_branch, pi-model branches like C2, generators on
     random buses, loads at `load_factor` of generation capacity.  Returns an
@@ -212,15 +213,16 @@ def grid(n_bus: int, n_branch: int, n_gen: int, seed: int = 4, load_factor: floa
     pd = load_factor * pmax.sum() * w / w.sum()
     qd = pd * u(n_bus, 0.1, 0.4)
     sh = u(n_bus) < shunt_frac
+    smax = u(n_branch, rate[0], rate[1])  # line ratings s-bar (per unit), used with line limits on
     return Grid(
         bus_pd=pd, bus_qd=qd, bus_gsh=np.where(sh, u(n_bus, 0.0, 0.01), 0.0),
         bus_bsh=np.where(sh, u(n_bus, 0.0, 0.1), 0.0), bus_vmin=np.full(n_bus, 0.9), bus_vmax=np.full(n_bus, 1.1),
         gen_bus=gen_bus, gen_c2=u(n_gen, 0.005, 0.05), gen_c1=u(n_gen, 1.0, 10.0), gen_pmin=np.zeros(n_gen),
         gen_pmax=pmax, gen_qmin=-0.5 * pmax, gen_qmax=0.5 * pmax, br_from=br_from, br_to=br_to,
-        br_coef=np.ascontiguousarray(coef))
+        br_coef=np.ascontiguousarray(coef), br_smax2=smax * smax)
 
 
-def two_bus(pd: float = 0.5, qd: float = 0.1, r: float = 0.01, x: float = 0.1):
+def two_bus(pd: float = 0.5, qd: float = 0.1, r: float = 0.01, x: float = 0.1, smax: float = None):
     """SPEC.md:411 single-branch 2-bus toy: one generator at bus 0, one load at bus 1."""
     from .admm import Grid
 
@@ -229,4 +231,5 @@ def two_bus(pd: float = 0.5, qd: float = 0.1, r: float = 0.01, x: float = 0.1):
                 bus_vmin=np.full(2, 0.9), bus_vmax=np.full(2, 1.1), gen_bus=np.array([0], np.int32),
                 gen_c2=np.array([0.1]), gen_c1=np.array([1.0]), gen_pmin=np.array([0.0]), gen_pmax=np.array([2.0]),
                 gen_qmin=np.array([-1.0]), gen_qmax=np.array([1.0]), br_from=np.array([0], np.int32),
-                br_to=np.array([1], np.int32), br_coef=np.ascontiguousarray(coef))
+                br_to=np.array([1], np.int32), br_coef=np.ascontiguousarray(coef),
+                br_smax2=None if smax is None else np.array([smax * smax]))

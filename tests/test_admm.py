@@ -158,6 +158,58 @@ def test_two_bus_toy_converges_and_matches_full_nlp():
     assert -1.0 <= qg <= 1.0
 
 
+# ------------------------------------------------------------ line limits
+def _binding_grid():
+    """A synthetic grid whose ratings bind: the d=4 (unlimited) ADMM flows
+    after 40 iterations, with s-bar = 0.7 |S| on the 15 % most loaded lines."""
+    g = synth.grid(150, 210, 40, seed=9, shunt_frac=0.3)
+    a = po.OracleAdmm(g)
+    for _ in range(40):
+        a.step()
+    x = a.get(A.BRANCH_X)
+    s = np.array([max(np.hypot(*synth.branch_flows(g.br_coef[l], *x[l])[0:2]),
+                      np.hypot(*synth.branch_flows(g.br_coef[l], *x[l])[2:4])) for l in range(g.n_branch)])
+    cut = np.quantile(s, 0.85)
+    g.br_smax2 = np.where(s >= cut, (0.7 * s) ** 2, 100.0)
+    return g, s >= cut
+
+
+def test_line_limits_enforced_by_auglag_loop():
+    """with line_limits the branch stage is the d=6
+    augmented-Lagrangian loop; the binding lines end feasible (|S| <= s-bar up
+    to the AL tolerance), the slacks stay in their boxes, and mu moved only on
+    the binding lines."""
+    g, bind = _binding_grid()
+    a = po.OracleAdmm(g, A.AdmmOptions(line_limits=True))
+    for _ in range(60):
+        a.step()
+    x = a.get(A.BRANCH_X)
+    assert x.shape == (g.n_branch, 6)
+    assert a.get(A.LINE_VIOL)[0] <= 1e-5
+    assert a.get(A.AUGLAG_ROUNDS)[0] > 60  # more than one round in some iterations
+    for l in range(g.n_branch):
+        f = synth.branch_flows(g.br_coef[l], *x[l, :4])
+        for e in range(2):
+            assert np.hypot(f[2 * e], f[2 * e + 1]) ** 2 <= g.br_smax2[l] + 1e-5
+            assert -g.br_smax2[l] <= x[l, 4 + e] <= 0.0
+    mu = a.get(A.BRANCH_PARAMS)[:, 32:34]
+    assert np.abs(mu[bind]).max() > 0.0
+    assert np.abs(mu[~bind]).max() < np.abs(mu[bind]).max()
+
+
+def test_line_limits_off_is_the_d4_spec_path():
+    """line_limits=False keeps the SPEC's 4-dimensional branch subproblem:
+    the ratings are ignored and no AL round runs."""
+    g = synth.grid(60, 80, 15, seed=3)
+    a, b = po.OracleAdmm(g), po.OracleAdmm(g, A.AdmmOptions(line_limits=False))
+    g.br_smax2 = None
+    c = po.OracleAdmm(g)
+    for _ in range(5):
+        assert a.step() == b.step() == c.step()
+    assert a.get(A.AUGLAG_ROUNDS)[0] == 0
+    assert a.get(A.BRANCH_X).shape == (g.n_branch, 4)
+
+
 # ------------------------------------------------------------ device
 @pytest.mark.gpu
 def test_device_admm_trajectory_bitwise_vs_oracle():
@@ -201,3 +253,20 @@ def test_sharded_path_world1_equals_single():
     for k in range(10):
         assert sh.step() == ref.step(), k
     assert np.array_equal(sh.solver.get(A.BRANCH_X), ref.get(A.BRANCH_X))
+
+
+@pytest.mark.gpu
+def test_device_admm_line_limits_bitwise_vs_oracle():
+    """The d=6 augmented-Lagrangian branch stage on the device (compaction of
+    the active branches, TRON, AL update kernel) against the oracle's loop:
+    residuals, every state array, the AL round count and the line violation
+    bit for bit."""
+    g, _ = _binding_grid()
+    opts = A.AdmmOptions(line_limits=True)
+    dev = A.AdmmSolver(g, opts)
+    cpu = po.OracleAdmm(g, opts, workers=8)
+    for k in range(20):
+        assert dev.step() == cpu.step(), f"iteration {k}"
+    for what in (A.GEN_P, A.GEN_Q, A.BUS_WT, A.BUS_TT, A.BRANCH_X, A.BRANCH_PARAMS, A.BRANCH_STATUS, A.COST,
+                 A.AUGLAG_ROUNDS, A.LINE_VIOL):
+        assert np.array_equal(dev.get(what), cpu.get(what)), what

@@ -67,7 +67,7 @@ def test_gloo_world2_sharded_equals_single_process():
         assert np.array_equal(v, getattr(ref, k)), k
 
 
-def _admm_worker(rank, world, port, q):
+def _admm_worker(rank, world, port, q, line_limits=False):
     """One rank of the sharded ADMM scheme (paper_2106_14995_b200/admm.py
     ShardedAdmm) with the CPU oracle as the compute backend and gloo as the
     collective: equal branch chunks, in-place all-gather of the branch
@@ -85,8 +85,12 @@ def _admm_worker(rank, world, port, q):
 
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
-    g = synth.grid(150, 210, 40, seed=9, shunt_frac=0.3)
-    a = po.OracleAdmm(g)
+    from paper_2106_14995_b200.admm import AdmmOptions
+
+    g = synth.grid(150, 210, 40, seed=9, shunt_frac=0.3, rate=(0.05, 0.6))
+    opts = AdmmOptions(line_limits=line_limits)
+    D = opts.branch_dim
+    a = po.OracleAdmm(g, opts)
     lib = a.lib
     lib.orc_admm_solve_components.argtypes = [C.c_void_p, C.c_int64, C.c_int64]
     lib.orc_admm_x.argtypes = [C.c_void_p]
@@ -96,14 +100,14 @@ def _admm_worker(rank, world, port, q):
     chunk = (g.n_branch + world - 1) // world
     lo, hi = min(g.n_branch, rank * chunk), min(g.n_branch, (rank + 1) * chunk)
     blo, bhi = partition(g.n_bus, world)[rank]
-    xs = np.ctypeslib.as_array(lib.orc_admm_x(a._h), shape=(g.n_branch * 4,))
-    buf = torch.zeros(chunk * world * 4, dtype=torch.float64)
+    xs = np.ctypeslib.as_array(lib.orc_admm_x(a._h), shape=(g.n_branch * D,))
+    buf = torch.zeros(chunk * world * D, dtype=torch.float64)
     hist = []
     for _ in range(12):
         assert lib.orc_admm_solve_components(a._h, lo, hi) == 0
-        buf[: g.n_branch * 4] = torch.from_numpy(xs)
-        dist.all_gather_into_tensor(buf, buf[rank * chunk * 4:(rank + 1) * chunk * 4].clone())
-        xs[:] = buf[: g.n_branch * 4].numpy()
+        buf[: g.n_branch * D] = torch.from_numpy(xs)
+        dist.all_gather_into_tensor(buf, buf[rank * chunk * D:(rank + 1) * chunk * D].clone())
+        xs[:] = buf[: g.n_branch * D].numpy()
         p, d = C.c_double(), C.c_double()
         lib.orc_admm_update_consensus(a._h, blo, bhi, C.byref(p), C.byref(d))
         r = torch.tensor([p.value, d.value], dtype=torch.float64)
@@ -115,20 +119,23 @@ def _admm_worker(rank, world, port, q):
     dist.destroy_process_group()
 
 
-def test_gloo_world2_sharded_admm_equals_single_process():
+@pytest.mark.parametrize("line_limits", [False, True])
+def test_gloo_world2_sharded_admm_equals_single_process(line_limits):
     from oracle import pyoracle as po
     from paper_2106_14995_b200 import synth
+    from paper_2106_14995_b200.admm import AdmmOptions
 
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_admm_worker, args=(r, 2, port, q)) for r in range(2)]
+    procs = [ctx.Process(target=_admm_worker, args=(r, 2, port, q, line_limits)) for r in range(2)]
     for p in procs:
         p.start()
     hist = q.get(timeout=180)
     for p in procs:
         p.join(timeout=180)
         assert p.exitcode == 0
-    a = po.OracleAdmm(synth.grid(150, 210, 40, seed=9, shunt_frac=0.3))
+    a = po.OracleAdmm(synth.grid(150, 210, 40, seed=9, shunt_frac=0.3, rate=(0.05, 0.6)),
+                      AdmmOptions(line_limits=line_limits))
     ref = [a.step() for _ in range(12)]
     assert hist == ref
