@@ -410,7 +410,9 @@ extern "C" int tb_solve_batch(tb_context* ctx, const tb_problem_batch* b, const 
                             (!in_host || (is_pinned(b->x0) && is_pinned(b->lower) && is_pinned(b->upper) &&
                                           (np == 0 || is_pinned(b->params)))) &&
                             (!out_host || (is_pinned(r->x_star) && is_pinned(r->f_star) && is_pinned(r->status)));
-        const int nch = (staged && n <= tbdev::max_warp_dim() && c >= 2 * kChunkMin)
+        size_t ws_need = 0;  // > 0: the persistent block kernel (one workspace per device): no chunking
+        CUDA_TRY(tbdev::tron_ws_need(b->family, n, c, &ws_need));
+        const int nch = (staged && ws_need == 0 && c >= 2 * kChunkMin)
                             ? (int)std::min<int64_t>(kMaxChunks, c / kChunkMin)
                             : 1;
         if (nch > 1) {

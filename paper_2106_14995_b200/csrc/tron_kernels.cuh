@@ -37,6 +37,17 @@ inline bool blk_asmem() {
     return e && e[0] == '1';
 }
 
+// smallest dimension routed to the block kernel: 21 (measured crossover on
+// ncvx, B = 32,768: d = 17 / 20 equal, d = 24 / 28 / 32 1.12x / 1.15x / 1.27x
+// faster on the D = 64 block kernel, whose compacted free systems allow two
+// parallel shift attempts where the D = 32 warp kernel runs one).  Override
+// with TB_BLOCK_MIN_DIM (17..33) for experiments.
+inline int blk_min_dim() {
+    const char* e = std::getenv("TB_BLOCK_MIN_DIM");
+    const int v = e ? std::atoi(e) : 21;
+    return v < 17 ? 17 : v;
+}
+
 // persistent grid: resident blocks per SM x SMs, capped by the batch
 template <int FAM, int D, bool ASMEM, bool COUNT>
 static cudaError_t blk_grid(long long count, long long* grid, size_t* smem_out) {
