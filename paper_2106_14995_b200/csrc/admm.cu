@@ -340,18 +340,23 @@ int tb_admm_solve_components(tb_admm* a, void* stream) {
     if (!a) return fail(TB_E_INVALID_ARGUMENT, "null admm");
     cudaSetDevice(a->device);
     cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : a->stream;
-    if (a->v.n_gen > 0) admm_gen_kernel<<<(a->v.n_gen + 127) / 128, 128, 0, st>>>(a->v);
+    if (a->v.n_gen > 0) {
+        admm_gen_kernel<<<(a->v.n_gen + 127) / 128, 128, 0, st>>>(a->v);
+        tbdev::note_launches(1);
+    }
     const int64_t cnt = a->br_hi - a->br_lo;
     if (cnt > 0 && a->dim == 6) {
         // augmented-Lagrangian rounds: solve the active branches, update mu / xi
         const unsigned gb = (unsigned)((cnt + 127) / 128);
         admm_auglag_reset_kernel<<<gb, 128, 0, st>>>(a->v.br_params, a->eta, a->active, a->br_lo, a->br_hi,
                                                      a->opt.auglag_xi0, a->opt.auglag_eta0);
+        tbdev::note_launches(1);
         for (int round = 0; round < a->opt.auglag_max_iter; ++round) {
             cudaMemsetAsync(a->cnt, 0, sizeof(int32_t), st);
             admm_auglag_gather_kernel<<<gb, 128, 0, st>>>(a->active, a->br_lo, a->br_hi, a->x, a->lower, a->upper,
                                                           a->v.br_params, a->cnt, a->cidx, a->cx, a->cl, a->cu,
                                                           a->cp);
+            tbdev::note_launches(1);
             int32_t nact = 0;
             cudaMemcpyAsync(&nact, a->cnt, sizeof nact, cudaMemcpyDeviceToHost, st);
             const cudaError_t e = cudaStreamSynchronize(st);
@@ -368,6 +373,7 @@ int tb_admm_solve_components(tb_admm* a, void* stream) {
             admm_auglag_update_kernel<<<(unsigned)((nact + 127) / 128), 128, 0, st>>>(
                 a->cnt, a->cidx, a->cxo, a->cst, a->x, a->status, a->v.br_params, a->eta, a->active,
                 a->opt.auglag_feas_tol, a->opt.auglag_xi_max);
+            tbdev::note_launches(1);
         }
     } else if (cnt > 0) {
         tb_problem_batch b{TB_FAMILY_BRANCH, 4, cnt, a->x + a->br_lo * 4, a->lower + a->br_lo * 4,
@@ -403,6 +409,7 @@ int tb_admm_update_consensus(tb_admm* a, void* stream, double* res2_dev) {
     cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : a->stream;
     cudaMemsetAsync(a->res, 0, 2 * sizeof(unsigned long long), st);
     admm_bus_kernel<<<(a->v.n_bus + 127) / 128, 128, 0, st>>>(a->v, a->bus_lo, a->bus_hi, a->res);
+    tbdev::note_launches(1);
     if (res2_dev) cudaMemcpyAsync(res2_dev, a->res, 2 * sizeof(double), cudaMemcpyDeviceToDevice, st);
     ++a->iterations;
     const cudaError_t e = cudaGetLastError();

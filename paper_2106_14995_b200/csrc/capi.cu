@@ -22,7 +22,6 @@
 namespace {
 
 thread_local std::string g_err;
-long long g_launches = 0;
 
 int set_err(int code, const char* fmt, ...) {
     char buf[1024];
@@ -89,7 +88,7 @@ struct tb_context {
 extern "C" {
 
 const char* tb_last_error(void) { return g_err.c_str(); }
-int64_t tb_kernel_launch_count(void) { return g_launches; }
+int64_t tb_kernel_launch_count(void) { return tbdev::launches(); }
 
 void tb_config_default(tb_tron_config* c) {
     std::memset(c, 0, sizeof(*c));
@@ -360,7 +359,6 @@ extern "C" int tb_solve_batch_async(tb_context* ctx, const tb_problem_batch* b, 
                                     b->params_stride, b->count, o);
     CUDA_TRY(attach_ws(d, b->family, a));
     CUDA_TRY(tbdev::launch_tron(b->family, a, st));
-    if (b->count > 0) ++g_launches;
     return TB_OK;
 }
 
@@ -468,7 +466,6 @@ extern "C" int tb_solve_batch(tb_context* ctx, const tb_problem_batch* b, const 
             CUDA_TRY(attach_ws(d, b->family, a));
             if (ch == 0) CUDA_TRY(cudaEventRecord(d.ev[1], st));
             CUDA_TRY(tbdev::launch_tron(b->family, a, st));
-            if (cc > 0) ++g_launches;
             if (ch == nch - 1 && nch == 1) CUDA_TRY(cudaEventRecord(d.ev[2], st));
             if (out_host && cc > 0) {
                 const int64_t h0 = g0;
@@ -536,6 +533,7 @@ extern "C" int tb_solve_batch(tb_context* ctx, const tb_problem_batch* b, const 
         CUDA_TRY(cudaMemcpyAsync(d.flag.p, &init, sizeof init, cudaMemcpyHostToDevice, d.stream));
         first_error_kernel<<<(unsigned)((c + 255) / 256), 256, 0, d.stream>>>(
             st_dev, c, static_cast<unsigned long long*>(d.flag.p));
+        tbdev::note_launches(1);
         unsigned long long idx = ~0ull;
         CUDA_TRY(cudaMemcpyAsync(&idx, d.flag.p, sizeof idx, cudaMemcpyDeviceToHost, d.stream));
         CUDA_TRY(cudaStreamSynchronize(d.stream));

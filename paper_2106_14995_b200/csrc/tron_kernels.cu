@@ -1,6 +1,8 @@
 // tron_kernels.cu — family dispatch of the TRON kernels.
 #include <cuda_runtime.h>
 
+#include <atomic>
+
 #include "tb_families.h"
 #include "tron_launch.h"
 
@@ -35,6 +37,10 @@ cudaError_t tron_ws_need(int family, int n, long long count, size_t* bytes) {
     }
     return cudaSuccess;
 }
+
+static std::atomic<long long> g_kernel_launches{0};
+void note_launches(long long k) { g_kernel_launches += k; }
+long long launches() { return g_kernel_launches.load(); }
 
 int max_warp_dim() { return 32; }
 int max_dim() { return 128; }

@@ -3,10 +3,12 @@
 #pragma once
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdlib>
 
 #include "tron_block.cuh"
 #include "tron_device.cuh"
+#include "tron_launch.h"
 
 namespace tbdev {
 
@@ -20,6 +22,7 @@ static cudaError_t launch_fdc(const KernelArgs& a, cudaStream_t st) {
         if (e != cudaSuccess) return e;
     }
     kern<<<(unsigned)a.count, 32, smem, st>>>(a);
+    note_launches(1);
     return cudaGetLastError();
 }
 
@@ -76,6 +79,7 @@ static cudaError_t launch_blk_c(const KernelArgs& a, cudaStream_t st) {
     if (!a.ws || a.ws_bytes < need) return cudaErrorMemoryAllocation;
     if ((e = cudaMemsetAsync(a.ws, 0, sizeof(unsigned), st)) != cudaSuccess) return e;
     tron_block_kernel<FAM, D, ASMEM, COUNT><<<(unsigned)grid, D, smem, st>>>(a);
+    note_launches(1);
     return cudaGetLastError();
 }
 
