@@ -42,7 +42,12 @@ namespace tbdev {
 template <int D, bool ASMEM>
 struct BlkLayout {
     static constexpr int NW = D / 32;
-    static constexpr int LP = D * (D + 1) / 2;      // packed factor, nf <= D
+    // shared factor region: every packed factor for nf <= D at D = 64; at
+    // D = 128 sized for 4 resident blocks per SM (2 parallel attempts at
+    // nf <= 64, one factor up to nf = 108); larger systems use the block's
+    // global fallback slice (LPFULL doubles)
+    static constexpr int LPFULL = D * (D + 1) / 2;
+    static constexpr int LP = D >= 128 ? 5888 : LPFULL;
     static constexpr int L = 0;
     static constexpr int RD = L + LP;                // RN(1 / L(p,p))
     static constexpr int S1 = RD + D;                // staging, double buffered
@@ -72,7 +77,8 @@ struct Blk {
     using SL = BlkLayout<D, ASMEM>;
     static constexpr int NW = SL::NW;
     double* A;       // D x D column-major (shared or global workspace)
-    double* L;       // packed lower factors, one per attempt group
+    double* L;       // packed lower factors, one per attempt group (shared)
+    double* Lglob;   // global fallback slice for factors beyond the shared region
     double* Lw;      // the successful attempt's factor
     double* RD;
     double* s1;
@@ -423,10 +429,12 @@ struct Blk {
         const int G = D / gt;
         const int gid = t / gt, p = t % gt;
         const int lpg = ((nf * (nf + 1)) / 2 + 1) & ~1;
-        double* Lg = L + gid * lpg;
+        // factors in the shared region when they fit, else the global slice
+        double* Lbase = G * lpg <= SL::LP ? L : Lglob;
+        double* Lg = Lbase + gid * lpg;
         // B = A[F,F] (lower triangle) staged once per call behind the G
         // factors when it fits: every attempt then reads shared memory
-        double* Bs = (G + 1) * lpg <= SL::LP ? L + G * lpg : nullptr;
+        double* Bs = (Lbase == L && (G + 1) * lpg <= SL::LP) ? L + G * lpg : nullptr;
         double dg = 0.0, ma = 0.0;
         if (t < nf) {
             const double* Ar = A + fidx[t];
@@ -480,7 +488,7 @@ struct Blk {
                 double sw = base;
                 for (int q = 0; q < winner; ++q) sw = tb_smax(2.0 * sw, alpha0);
                 shift = sw;
-                Lw = L + winner * lpg;
+                Lw = Lbase + winner * lpg;
                 if (t < nf) RD[t] = 1.0 / Lat(t, t);
                 sync();
                 return 0;
@@ -995,10 +1003,25 @@ struct BlkFamily {
 // a.ws: the work counter (first 256 bytes), then one D x D Hessian slice per
 // block (global variant).
 constexpr size_t kBlkWsHeader = 256;
+#ifndef TB_BLK_MIN128
+#define TB_BLK_MIN128 4
+#endif
+#ifndef TB_BLK_MIN64
+#define TB_BLK_MIN64 8
+#endif
 template <int D>
 struct BlkMinBlocks {
-    static constexpr int value = D >= 128 ? 3 : 8;
+    static constexpr int value = D >= 128 ? TB_BLK_MIN128 : TB_BLK_MIN64;
 };
+// ws = header | A slices (grid x D^2, global-A variant) | factor fallback
+// slices (grid x LPFULL, D = 128 only)
+template <int D>
+__device__ __forceinline__ double* blk_lglob(const KernelArgs& a, bool asmem) {
+    double* base = reinterpret_cast<double*>(static_cast<char*>(a.ws) + kBlkWsHeader);
+    if (!asmem) base += (size_t)gridDim.x * D * D;
+    return base + (size_t)blockIdx.x * (D * (D + 1) / 2);
+}
+
 template <int FAM, int D, bool ASMEM, bool COUNT>
 __global__ void __launch_bounds__(D, BlkMinBlocks<D>::value) tron_block_kernel(const __grid_constant__ KernelArgs a) {
     extern __shared__ double smem[];
@@ -1009,6 +1032,7 @@ __global__ void __launch_bounds__(D, BlkMinBlocks<D>::value) tron_block_kernel(c
                 : reinterpret_cast<double*>(static_cast<char*>(a.ws) + kBlkWsHeader) + (size_t)blockIdx.x * D * D;
     W.L = smem + SL::L;
     W.Lw = W.L;
+    W.Lglob = SL::LP < SL::LPFULL ? blk_lglob<D>(a, ASMEM) : nullptr;
     W.RD = smem + SL::RD;
     W.s1 = smem + SL::S1;
     W.s2 = smem + SL::S2;

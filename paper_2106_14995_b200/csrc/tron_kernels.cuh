@@ -75,7 +75,9 @@ static cudaError_t launch_blk_c(const KernelArgs& a, cudaStream_t st) {
     size_t smem = 0;
     cudaError_t e = blk_grid<FAM, D, ASMEM, COUNT>(a.count, &grid, &smem);
     if (e != cudaSuccess) return e;
-    const size_t need = kBlkWsHeader + (ASMEM ? 0 : sizeof(double) * (size_t)grid * D * D);
+    using SL = BlkLayout<D, ASMEM>;
+    const size_t need = kBlkWsHeader + (ASMEM ? 0 : sizeof(double) * (size_t)grid * D * D) +
+                        (SL::LP < SL::LPFULL ? sizeof(double) * (size_t)grid * SL::LPFULL : 0);
     if (!a.ws || a.ws_bytes < need) return cudaErrorMemoryAllocation;
     if ((e = cudaMemsetAsync(a.ws, 0, sizeof(unsigned), st)) != cudaSuccess) return e;
     tron_block_kernel<FAM, D, ASMEM, COUNT><<<(unsigned)grid, D, smem, st>>>(a);
@@ -96,13 +98,18 @@ static cudaError_t ws_need_blk(long long count, size_t* bytes) {
     long long grid = 0;
     size_t smem = 0;
     *bytes = kBlkWsHeader;
-    if (blk_asmem()) return cudaSuccess;
-    cudaError_t e = blk_grid<FAM, D, false, false>(count, &grid, &smem);
+    const bool as = blk_asmem();
+    cudaError_t e = as ? blk_grid<FAM, D, true, false>(count, &grid, &smem)
+                       : blk_grid<FAM, D, false, false>(count, &grid, &smem);
     if (e != cudaSuccess) return e;
     long long g2 = 0;
-    if ((e = blk_grid<FAM, D, false, true>(count, &g2, &smem)) != cudaSuccess) return e;
+    if ((e = as ? blk_grid<FAM, D, true, true>(count, &g2, &smem) : blk_grid<FAM, D, false, true>(count, &g2, &smem)) !=
+        cudaSuccess)
+        return e;
     if (g2 > grid) grid = g2;
-    *bytes += sizeof(double) * (size_t)grid * D * D;
+    using SL = BlkLayout<D, false>;
+    if (!as) *bytes += sizeof(double) * (size_t)grid * D * D;
+    if (SL::LP < SL::LPFULL) *bytes += sizeof(double) * (size_t)grid * SL::LPFULL;
     return cudaSuccess;
 }
 
