@@ -10,6 +10,7 @@
 #include <chrono>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -261,7 +262,12 @@ bool is_pinned(const void* p) {
     }
     return at.type == cudaMemoryTypeHost;
 }
-constexpr int64_t kMaxChunks = 8;
+constexpr int64_t kMaxChunks = 4;  // measured on C2 e2e: 1 / 2 / 4 / 8 chunks 10.41 / 10.10 / 9.55 / 9.81 ms
+int64_t max_chunks() {  // TB_CHUNKS overrides (experiments); 1 disables the pipeline
+    const char* e = std::getenv("TB_CHUNKS");
+    const int64_t v = e ? std::atoll(e) : kMaxChunks;
+    return v < 1 ? 1 : (v > kMaxChunks ? kMaxChunks : v);
+}
 
 struct OutPtrs {
     double *x_star, *f_star, *pg;
@@ -339,6 +345,49 @@ cudaError_t attach_ws(DevState& d, int family, tbdev::KernelArgs& a) {
     return cudaSuccess;
 }
 
+// Device-resident batch on the warp kernel: `nch` concurrent chunk launches
+// forked from `st` onto the device's chunk streams and joined back, so the
+// long-running problems of one chunk overlap the bulk of the others (the
+// launch finishes with its slowest problem).
+cudaError_t launch_split(DevState& d, int family, const tbdev::KernelArgs& a, cudaStream_t st, int nch) {
+    if (nch <= 1) return tbdev::launch_tron(family, a, st);
+    cudaError_t e = cudaEventRecord(d.fork, st);
+    for (int k = 0; k < nch && e == cudaSuccess; ++k) e = cudaStreamWaitEvent(d.aux[k], d.fork, 0);
+    for (int k = 0; k < nch && e == cudaSuccess; ++k) {
+        const int64_t a0 = a.count * k / nch, a1 = a.count * (k + 1) / nch;
+        tbdev::KernelArgs c = a;
+        const int n = a.n;
+        c.count = a1 - a0;
+        c.x0 += a0 * n;
+        c.lo += a0 * n;
+        c.up += a0 * n;
+        if (c.prm) c.prm += a0 * a.stride;
+        if (c.x_star) c.x_star += a0 * n;
+        if (c.f_star) c.f_star += a0;
+        if (c.pg_norm) c.pg_norm += a0;
+        if (c.status) c.status += a0;
+        if (c.iterations) c.iterations += a0;
+        if (c.cg_iterations) c.cg_iterations += a0;
+        if (c.f_evals) c.f_evals += a0;
+        if (c.wall_time) c.wall_time += a0;
+        if (c.flops) c.flops += a0;
+        e = tbdev::launch_tron(family, c, d.aux[k]);
+    }
+    for (int k = 0; k < nch && e == cudaSuccess; ++k) {
+        e = cudaEventRecord(d.join, d.aux[k]);
+        if (e == cudaSuccess) e = cudaStreamWaitEvent(st, d.join, 0);
+    }
+    return e;
+}
+
+// chunk count of a device-resident batch (warp kernel only: the persistent
+// block kernel owns one workspace per device)
+int device_chunks(int family, int n, int64_t count) {
+    size_t need = 0;
+    if (tbdev::tron_ws_need(family, n, count, &need) != cudaSuccess || need != 0) return 1;
+    return count >= 2 * kChunkMin ? (int)std::min<int64_t>(max_chunks(), count / kChunkMin) : 1;
+}
+
 }  // namespace
 
 extern "C" int tb_solve_batch_async(tb_context* ctx, const tb_problem_batch* b, const tb_tron_config* cfg,
@@ -358,7 +407,7 @@ extern "C" int tb_solve_batch_async(tb_context* ctx, const tb_problem_batch* b, 
     tbdev::KernelArgs a = make_args(b, np, cfg, ctx->fast_forward, b->x0, b->lower, b->upper, b->params,
                                     b->params_stride, b->count, o);
     CUDA_TRY(attach_ws(d, b->family, a));
-    CUDA_TRY(tbdev::launch_tron(b->family, a, st));
+    CUDA_TRY(launch_split(d, b->family, a, st, device_chunks(b->family, b->dim, b->count)));
     return TB_OK;
 }
 
@@ -411,7 +460,7 @@ extern "C" int tb_solve_batch(tb_context* ctx, const tb_problem_batch* b, const 
         size_t ws_need = 0;  // > 0: the persistent block kernel (one workspace per device): no chunking
         CUDA_TRY(tbdev::tron_ws_need(b->family, n, c, &ws_need));
         const int nch = (staged && ws_need == 0 && c >= 2 * kChunkMin)
-                            ? (int)std::min<int64_t>(kMaxChunks, c / kChunkMin)
+                            ? (int)std::min<int64_t>(max_chunks(), c / kChunkMin)
                             : 1;
         if (nch > 1) {
             CUDA_TRY(cudaEventRecord(d.fork, d.stream));
@@ -428,6 +477,7 @@ extern "C" int tb_solve_batch(tb_context* ctx, const tb_problem_batch* b, const 
         if (out_host) {
             CUDA_TRY(d.out.ensure(out_bytes(c, n)));
             ofull = carve(d.out.p, c, n);
+            if (!r->flops) ofull.flops = nullptr;  // non-null flops selects the counting kernel variant
         } else {
             ofull = OutPtrs{r->x_star, r->f_star, r->pg_norm, r->status, r->iterations, r->cg_iterations,
                             r->f_evals, r->flops, r->wall_time};
@@ -465,7 +515,8 @@ extern "C" int tb_solve_batch(tb_context* ctx, const tb_problem_batch* b, const 
             tbdev::KernelArgs a = make_args(b, np, cfg, ctx->fast_forward, x0, lw, up, prm, stride, cc, o);
             CUDA_TRY(attach_ws(d, b->family, a));
             if (ch == 0) CUDA_TRY(cudaEventRecord(d.ev[1], st));
-            CUDA_TRY(tbdev::launch_tron(b->family, a, st));
+            if (!staged) CUDA_TRY(launch_split(d, b->family, a, st, device_chunks(b->family, n, cc)));
+            else CUDA_TRY(tbdev::launch_tron(b->family, a, st));
             if (ch == nch - 1 && nch == 1) CUDA_TRY(cudaEventRecord(d.ev[2], st));
             if (out_host && cc > 0) {
                 const int64_t h0 = g0;
