@@ -435,9 +435,9 @@ def main():
         dist.all_reduce(e2e_t, op=dist.ReduceOp.MAX)
     e2e_value = world * N / float(e2e_t.item())
     h2d = sum(a.nbytes for a in (hbatch.x0, hbatch.lower, hbatch.upper, hbatch.params))
+    # every SolveReport field + per-problem device time (flops are not requested, so not copied)
     d2h = (hout.x_star.nbytes + hout.f_star.nbytes + hout.pg_norm.nbytes + hout.status.nbytes +
-           hout.iterations.nbytes + hout.cg_iterations.nbytes + hout.f_evals.nbytes + hout.per_problem_time.nbytes +
-           hout.flops.nbytes)
+           hout.iterations.nbytes + hout.cg_iterations.nbytes + hout.f_evals.nbytes + hout.per_problem_time.nbytes)
 
     # ---- CPU baseline (rank 0, N=1 only): the reference's solve_batch
     cpu = None
