@@ -272,3 +272,58 @@ def test_cpp_dropin_against_reference_solve_batch():
     p = subprocess.run([exe], capture_output=True, text=True, timeout=300)
     assert p.returncode == 0, p.stdout + p.stderr
     assert '"failed": 0' in p.stdout
+
+
+# --------------------------------------- block kernel (d >= 21): edge cases
+@pytest.mark.parametrize("cfg", [TronConfig(max_iter=1), TronConfig(delta0=0.3), TronConfig(tol_pg=1e-9),
+                                 TronConfig(cg_tol=0.5, mu0=0.1, interp_factor=0.25),
+                                 TronConfig(sigma1=0.1, sigma2=0.3, sigma3=2.0, eta0=0.01, delta_max=5.0)])
+def test_block_kernel_config_variants_bitwise(solver, cfg):
+    for b in (synth.ncvx(48, 24, seed=4), synth.ncvx(16, 70, seed=4), synth.hs45(2, 40)):
+        assert_bitwise(solver.solve_batch(b, cfg=cfg), po.solve_batch(b, cfg=cfg, impl="oracle", workers=8),
+                       label=f"d={b.dim} {cfg}")
+
+
+def test_block_kernel_outside_box_and_infinite_bounds(solver):
+    b = synth.boxqp(64, 40, seed=8)
+    b.lower[::3, 1] = -np.inf
+    b.upper[::4, 2] = np.inf
+    x0 = b.x0 * 5.0
+    res = solver.solve_batch(b, x0)
+    assert_bitwise(res, po.solve_batch(b, x0, impl="oracle", workers=8), label="block outside/inf")
+
+
+@pytest.mark.parametrize("d", [24, 40, 100])
+def test_block_kernel_nan_hessian_factorization_failed(solver, d):
+    """tron_test.cpp:251-266 at block-kernel sizes: a NaN diagonal entry with
+    a zero gradient component -> FactorizationFailed at iteration 1."""
+    H = np.eye(d).ravel(order="F")
+    H[(d - 1) + (d - 1) * d] = np.nan
+    c = np.zeros(d)
+    c[-1] = 0.5
+    prm = np.tile(np.concatenate([H, c]), (3, 1))
+    b = ProblemBatch(1, d, np.full((3, d), -1.0), np.full((3, d), 1.0), prm, np.tile(np.full(d, 0.5), (3, 1)))
+    b.x0[:, -1] = 0.5
+    res = solver.solve_batch(b)
+    assert_bitwise(res, po.solve_batch(b, impl="oracle"), label=f"nan hessian d={d}")
+    assert (host(res.status) == SolveStatus.FactorizationFailed).all()
+
+
+def test_block_kernel_evaluation_error_and_invalid_bounds(solver):
+    b = synth.boxqp(4, 30, seed=6)
+    b.params[2, 0] = np.inf
+    with pytest.raises(EvaluationError):
+        solver.solve_batch(b)
+    b = synth.ncvx(4, 50)
+    b.lower[1, 0] = b.upper[1, 0] + 1.0
+    with pytest.raises(ValueError, match="lower bound exceeds upper bound"):
+        solver.solve_batch(b)
+
+
+@pytest.mark.parametrize("count", [0, 1, 3])
+def test_block_kernel_tiny_batches(solver, count):
+    b = synth.ncvx(count, 64, seed=12)
+    res = solver.solve_batch(b)
+    assert host(res.status).shape == (count,)
+    if count:
+        assert_bitwise(res, po.solve_batch(b, impl="oracle"), label=f"count={count}")
