@@ -89,6 +89,36 @@ int main() {
             for (int i = 0; i < n; ++i) CHECK(std::fabs(g.reports[0].x_star[i] - (i + 1)) <= 1e-6);
         }
     }
+    // block-kernel sizes (d > 20): indefinite box QPs at d = 24 / 48 / 100 and
+    // hs45 up to the reference's capacity (batch.hpp:15, 64), bitwise
+    for (int n : {24, 48, 100}) {
+        std::vector<gpu::FamilyProblem<TB_FAMILY_BOXQP>> gp;
+        std::vector<FunctionProblem> rp;
+        std::vector<Vector> x0s;
+        for (int t = 0; t < (n > 64 ? 6 : 24); ++t) {
+            DenseMatrix h(n);
+            for (int j = 0; j < n; ++j)
+                for (int i = j; i < n; ++i) h(i, j) = h(j, i) = testutil::uniform(-1.0, 1.0);
+            Vector c = testutil::random_vector(n, -1.5, 1.5);
+            Vector l(n), u(n);
+            for (int i = 0; i < n; ++i) {
+                l[i] = testutil::uniform(-1.5, -0.5);
+                u[i] = testutil::uniform(0.5, 1.5);
+            }
+            gp.push_back(gpu::make_quadratic(h, c, l, u));
+            rp.push_back(testutil::make_quadratic(h, c, l, u));
+            x0s.push_back(testutil::random_vector(n, -0.5, 0.5));
+        }
+        const BatchResult g = gpu::solve_batch(gp, x0s, TronConfig{}, ctx);
+        const BatchResult r = solve_batch(rp, x0s, TronConfig{}, 4);
+        same_reports(g, r, ("indefinite box QPs d=" + std::to_string(n)).c_str());
+    }
+    for (int n : {33, 64}) {
+        const BatchResult g = gpu::solve_batch(std::vector{gpu::make_hs45(n)},
+                                               std::vector<Vector>{make_hs45(n).default_start()}, TronConfig{}, ctx);
+        const BatchResult r = solve_batch(std::vector{make_hs45(n)}, std::vector<Vector>{make_hs45(n).default_start()});
+        same_reports(g, r, ("hs45 n=" + std::to_string(n)).c_str());
+    }
     // tron_test.cpp:251-266: NaN Hessian surfaces as FactorizationFailed
     {
         DenseMatrix h(2);
