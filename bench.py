@@ -248,7 +248,7 @@ C3_DIMS = (4, 8, 16, 32, 64, 128)
 C3_BATCH = 32768
 
 
-def run_sweep(args, dev):
+def run_sweep(args, dev, fp64_peak=None):
     """C1 (1,024 ncvx d=4) and the C3 dimension sweep (ncvx, batch 32,768,
     d = 4..128): device time of one batched solve with inputs in HBM (median
     of `reps` after a warm-up) next to the reference's CPU solve_batch on a
@@ -281,7 +281,11 @@ def run_sweep(args, dev):
             solver.solve_batch(db, out=out_d)
             ks.append(out_d.kernel_time)
         ms = 1e3 * statistics.median(ks)
+        # algorithmic flops of the same batch (untimed counting variant, identical results)
+        solver.solve_batch(db, out=out_d, count_flops=True)
+        flops = float(out_d.flops.sum().item())
         row = {"config": name, "family": "ncvx", "dim": d, "batch": B, "ms": ms, "solves_per_s": B / (ms * 1e-3),
+               "achieved_tflops": flops / (ms * 1e-3) / 1e12, "flops_per_solve": flops / B,
                "kernel": "warp per problem" if d <= 32 else f"block of {64 if d <= 64 else 128} threads (persistent)",
                "mean_iterations": float(out_d.iterations.double().mean().item()),
                "status_counts": {str(k): int(v) for k, v in
@@ -294,6 +298,8 @@ def run_sweep(args, dev):
             row["cpu_baseline"] = {"value": v, "unit": "solves/s", "cores": cores, "kind": "reference",
                                    "sample": f"first {n} of the {B} problems, reference solve_batch(workers={cores})"}
             row["speedup_vs_cpu"] = row["solves_per_s"] / v
+        if fp64_peak:
+            row["roofline_frac"] = row["achieved_tflops"] / fp64_peak
         out.append(row)
         del db, out_d, b
         torch.cuda.empty_cache()
@@ -461,7 +467,7 @@ def main():
     sweep = None
     if rank == 0 and world == 1 and not args.no_sweep:
         try:
-            sweep = run_sweep(args, dev)
+            sweep = run_sweep(args, dev, fp64_peak)
         except Exception as e:
             sweep = [{"error": repr(e)}]
 
