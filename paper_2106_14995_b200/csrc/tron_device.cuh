@@ -46,7 +46,7 @@
 #define TB_SOLVE_INLINE __forceinline__
 #endif
 #ifndef TB_MIN_BLOCKS
-#define TB_MIN_BLOCKS 16  // resident one-warp blocks per SM the register budget targets
+#define TB_MIN_BLOCKS 0  // > 0: force this many resident one-warp blocks per SM for every D
 #endif
 
 // Debug build only (-DTB_PHASES): per-phase clock64() accumulation, read back
@@ -846,9 +846,24 @@ __device__ __forceinline__ unsigned long long globaltimer() {
     return t;
 }
 
+// Resident one-warp blocks per SM the register budget targets (the kernel is
+// latency-bound and its SM throughput grows with resident warps; a few
+// spilled registers cost less than the lost residency).  Measured on B200,
+// device-resident batches: D=6 C2 9.56 / 8.89 / 8.43 / 8.28 /
+// 9.14 ms at 16 / 18 / 22 / 24 / 28; D=4 and D=8 best at 22, D=16 at 20.
+template <int D>
+struct WarpMinBlocks {
+    static constexpr int value = TB_MIN_BLOCKS > 0 ? TB_MIN_BLOCKS
+                                 : D <= 4          ? 22
+                                 : D <= 6          ? 24
+                                 : D <= 8          ? 22
+                                 : D <= 16         ? 20
+                                                   : 16;
+};
+
 // tron.hpp:453-549 solve(), one problem per warp (one warp per block).
 template <int FAM, int D, bool COUNT>
-__global__ void __launch_bounds__(32, TB_MIN_BLOCKS) tron_solve_kernel(const __grid_constant__ KernelArgs a) {
+__global__ void __launch_bounds__(32, WarpMinBlocks<D>::value) tron_solve_kernel(const __grid_constant__ KernelArgs a) {
     extern __shared__ double smem[];
     using SL = SmemLayout<D>;
     const long long pid = blockIdx.x;
