@@ -200,6 +200,7 @@ def run_admm(args, rank, world, local, dev):
         dist.all_reduce(ms, op=dist.ReduceOp.MAX)
     ms_iter = float(ms.item()) / args.admm_iters
     line = {"metric": "ADMM iterations/sec", "value": 1e3 / ms_iter, "unit": "iter/s", "ms_per_iter": ms_iter,
+            "scaling": "strong" if world > 1 else None,  # C5: one fixed grid sharded over N GPUs
             "iters_timed": args.admm_iters, "warmup_iters": max(3, args.warmup),
             "config": {"workload": cfg, "n_bus": grid.n_bus, "n_branch": grid.n_branch, "n_gen": grid.n_gen,
                        "branch_dim": 4, "parallelism": f"branches sharded over {world} GPU(s), NCCL all-gather"},
