@@ -35,7 +35,8 @@
 #include "tb_flops.h"
 
 #ifndef TB_UNROLL_MAX
-#define TB_UNROLL_MAX 8  // fully unroll the D-loops of kernels with D <= this
+#define TB_UNROLL_MAX 6  // fully unroll the D-loops of kernels with D <= this (D = 8: masked loops,
+                         // fewer live registers: ncvx8 6.09 -> 4.00 ms at 24 blocks/SM)
 #endif
 #ifndef TB_OUTLINE_SOLVES
 #define TB_OUTLINE_SOLVES 0  // 1: one out-of-line copy of each triangular solve (measured slower)
@@ -850,13 +851,14 @@ __device__ __forceinline__ unsigned long long globaltimer() {
 // latency-bound and its SM throughput grows with resident warps; a few
 // spilled registers cost less than the lost residency).  Measured on B200,
 // device-resident batches: D=6 C2 9.56 / 8.89 / 8.43 / 8.28 /
-// 9.14 ms at 16 / 18 / 22 / 24 / 28; D=4 and D=8 best at 22, D=16 at 20.
+// 9.14 ms at 16 / 18 / 22 / 24 / 28; D=4 best at 22, D=8 (masked loops) at
+// 24 (4.00 / 4.58 / 4.49 ms at 24 / 28 / 32), D=16 at 20.
 template <int D>
 struct WarpMinBlocks {
     static constexpr int value = TB_MIN_BLOCKS > 0 ? TB_MIN_BLOCKS
                                  : D <= 4          ? 22
                                  : D <= 6          ? 24
-                                 : D <= 8          ? 22
+                                 : D <= 8          ? 24
                                  : D <= 16         ? 20
                                                    : 16;
 };
