@@ -37,6 +37,13 @@
 
 #include "tron_device.cuh"
 
+#ifndef TB_BLK_MIN128
+#define TB_BLK_MIN128 4  // resident D = 128 blocks per SM (registers / shared factor region)
+#endif
+#ifndef TB_BLK_MIN64
+#define TB_BLK_MIN64 8
+#endif
+
 namespace tbdev {
 
 template <int D, bool ASMEM>
@@ -47,7 +54,7 @@ struct BlkLayout {
     // nf <= 64, one factor up to nf = 108); larger systems use the block's
     // global fallback slice (LPFULL doubles)
     static constexpr int LPFULL = D * (D + 1) / 2;
-    static constexpr int LP = D >= 128 ? 5888 : LPFULL;
+    static constexpr int LP = D >= 128 ? (TB_BLK_MIN128 >= 5 ? 4352 : 5888) : LPFULL;
     static constexpr int L = 0;
     static constexpr int RD = L + LP;                // RN(1 / L(p,p))
     static constexpr int S1 = RD + D;                // staging, double buffered
@@ -1003,12 +1010,6 @@ struct BlkFamily {
 // a.ws: the work counter (first 256 bytes), then one D x D Hessian slice per
 // block (global variant).
 constexpr size_t kBlkWsHeader = 256;
-#ifndef TB_BLK_MIN128
-#define TB_BLK_MIN128 4
-#endif
-#ifndef TB_BLK_MIN64
-#define TB_BLK_MIN64 8
-#endif
 template <int D>
 struct BlkMinBlocks {
     static constexpr int value = D >= 128 ? TB_BLK_MIN128 : TB_BLK_MIN64;
