@@ -327,3 +327,18 @@ def test_block_kernel_tiny_batches(solver, count):
     assert host(res.status).shape == (count,)
     if count:
         assert_bitwise(res, po.solve_batch(b, impl="oracle"), label=f"count={count}")
+
+
+@pytest.mark.parametrize("d", [100, 128])
+def test_block_kernel_large_free_systems_use_global_factor_slice(solver, d):
+    """Wide bounds keep every variable free (nf = d > 108 at D = 128): the
+    factor no longer fits the shared region and lives in the block's global
+    fallback slice; results stay bit-identical."""
+    # convex (one Newton step) and indefinite box QPs (several faces at nf = d)
+    for b in (synth.boxqp(6, d, seed=d), synth.boxqp(6, d, seed=d + 1, spd_boost=-0.3)):
+        b.lower[:] = -50.0
+        b.upper[:] = 50.0
+        res = solver.solve_batch(b, count_flops=True)
+        ref = po.solve_batch(b, impl="oracle", workers=6)
+        assert_bitwise(res, ref, label=f"wide bounds d={d} fam={b.family}")
+        assert np.array_equal(host(res.flops), ref.flops)
