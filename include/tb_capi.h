@@ -131,7 +131,10 @@ int tb_context_set_mode(tb_context* ctx, int32_t mode, int32_t fast_forward);
 
 /* solve_batch (batch.hpp:27-78): blocking.  Returns TB_E_PROBLEM if any
  * problem reports a status >= TB_STATUS_EVALUATION_ERROR (the reference would
- * have thrown); results are still written. */
+ * have thrown); results are still written.  Dimensions 1..128: one warp per
+ * problem up to d = 20, a block of 64 / 128 threads per problem above
+ * (persistent grid, workspace owned by the context); larger d is rejected with
+ * TB_E_INVALID_ARGUMENT. */
 int tb_solve_batch(tb_context* ctx, const tb_problem_batch* batch, const tb_tron_config* cfg,
                    tb_batch_result* result);
 /* Stream-ordered variant for device-resident batches on a single-device
@@ -145,7 +148,8 @@ int tb_imbalance(const double* times, int32_t n_iters, int32_t n_parts, double* 
                  double* nu_max, double* nu_min, double* nu_mean);
 
 const char* tb_last_error(void);
-/* Number of solver-kernel launches issued since load (evidence counter). */
+/* Number of kernels this library launched since load (TRON, block, error
+ * scan and ADMM stage kernels; evidence counter for the bench). */
 int64_t tb_kernel_launch_count(void);
 
 /* FP64 DFMA throughput of `device` in TFLOP/s (the roofline denominator of
