@@ -408,7 +408,8 @@ int tb_admm_update_consensus(tb_admm* a, void* stream, double* res2_dev) {
     cudaSetDevice(a->device);
     cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : a->stream;
     cudaMemsetAsync(a->res, 0, 2 * sizeof(unsigned long long), st);
-    admm_bus_kernel<<<(a->v.n_bus + 127) / 128, 128, 0, st>>>(a->v, a->bus_lo, a->bus_hi, a->res);
+    // 32-thread blocks: one bus per thread with serial per-bus work, spread over every SM
+    admm_bus_kernel<<<(a->v.n_bus + 31) / 32, 32, 0, st>>>(a->v, a->bus_lo, a->bus_hi, a->res);
     tbdev::note_launches(1);
     if (res2_dev) cudaMemcpyAsync(res2_dev, a->res, 2 * sizeof(double), cudaMemcpyDeviceToDevice, st);
     ++a->iterations;
