@@ -262,11 +262,16 @@ bool is_pinned(const void* p) {
     }
     return at.type == cudaMemoryTypeHost;
 }
-constexpr int64_t kMaxChunks = 4;  // measured on C2 e2e: 1 / 2 / 4 / 8 chunks 10.41 / 10.10 / 9.55 / 9.81 ms
-int64_t max_chunks() {  // TB_CHUNKS overrides (experiments); 1 disables the pipeline
+// chunk counts (measured on C2 at 24 blocks/SM, 10-step bench): host-staged
+// e2e 7.18 / 7.45 / 7.54 / 7.58 / 7.95 / 8.11 M solves/s at 1 / 2 / 3 / 4 / 6 /
+// 8 chunks (smaller first H2D, finer copy/compute overlap); device-resident
+// 8.32 / 8.65 / 8.34 / 8.25 / 8.28 / 8.41 ms -> 4.
+constexpr int64_t kHostChunks = 8;
+constexpr int64_t kDeviceChunks = 4;
+int64_t max_chunks(bool host) {  // TB_CHUNKS overrides both (experiments); 1 disables the split
     const char* e = std::getenv("TB_CHUNKS");
-    const int64_t v = e ? std::atoll(e) : kMaxChunks;
-    return v < 1 ? 1 : (v > kMaxChunks ? kMaxChunks : v);
+    const int64_t v = e ? std::atoll(e) : (host ? kHostChunks : kDeviceChunks);
+    return v < 1 ? 1 : (v > 8 ? 8 : v);  // one stream per chunk: aux[8]
 }
 
 struct OutPtrs {
@@ -385,7 +390,7 @@ cudaError_t launch_split(DevState& d, int family, const tbdev::KernelArgs& a, cu
 int device_chunks(int family, int n, int64_t count) {
     size_t need = 0;
     if (tbdev::tron_ws_need(family, n, count, &need) != cudaSuccess || need != 0) return 1;
-    return count >= 2 * kChunkMin ? (int)std::min<int64_t>(max_chunks(), count / kChunkMin) : 1;
+    return count >= 2 * kChunkMin ? (int)std::min<int64_t>(max_chunks(false), count / kChunkMin) : 1;
 }
 
 }  // namespace
@@ -460,7 +465,7 @@ extern "C" int tb_solve_batch(tb_context* ctx, const tb_problem_batch* b, const 
         size_t ws_need = 0;  // > 0: the persistent block kernel (one workspace per device): no chunking
         CUDA_TRY(tbdev::tron_ws_need(b->family, n, c, &ws_need));
         const int nch = (staged && ws_need == 0 && c >= 2 * kChunkMin)
-                            ? (int)std::min<int64_t>(max_chunks(), c / kChunkMin)
+                            ? (int)std::min<int64_t>(max_chunks(true), c / kChunkMin)
                             : 1;
         if (nch > 1) {
             CUDA_TRY(cudaEventRecord(d.fork, d.stream));
