@@ -223,7 +223,7 @@ def run_admm(args, rank, world, local, dev):
             "value": 1.0 / dt, "unit": "iter/s", "ms_per_iter": 1e3 * dt, "iters_timed": k,
             "auglag_rounds_per_iter": (int(ll.get(A.AUGLAG_ROUNDS)[0]) - r0) / k,
             "max_line_violation": float(ll.get(A.LINE_VIOL)[0]), "branch_dim": 6,
-            "timing": "host wall clock per blocking tb_admm_step (the AL loop reads the active count every round)"}
+            "timing": "host wall clock per blocking tb_admm_step (branch stage = one fused augmented-Lagrangian launch)"}
         ll.close()
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:

@@ -3,7 +3,9 @@
 //
 // Per iteration, all on the device of this process:
 //   admm_gen_kernel        generator closed form (all generators)
-//   tron_solve_kernel      branch subproblems of this shard (warm start, in place)
+//   tron_solve_kernel      branch subproblems of this shard (warm start, in place);
+//                          with line limits admm_auglag_fused_kernel runs each
+//                          branch's augmented-Lagrangian loop in one launch
 //   [exchange]             the caller all-gathers the branch solutions x
 //                          (NCCL over NVLink when sharded; nothing when not)
 //   admm_bus_kernel        bus consensus + multipliers + residual terms (every
@@ -61,44 +63,48 @@ __global__ void admm_cost_kernel(tb_admm_view v, double* out) {
     }
 }
 
-// ---- line limits: augmented-Lagrangian rounds over this shard's branches
-__global__ void admm_auglag_reset_kernel(double* prm, double* eta, int32_t* active, int64_t lo, int64_t hi,
-                                         double xi0, double eta0) {
-    const int64_t l = lo + blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (l >= hi) return;
-    prm[l * TB_BR_NPARAMS + TB_BR_XI] = xi0;
-    eta[l] = eta0;
-    active[l] = 1;
-}
-
-// compact the active branches of [lo, hi) into a dense TRON batch (slot order
-// is arbitrary: every problem's result is independent of its position)
-__global__ void admm_auglag_gather_kernel(const int32_t* active, int64_t lo, int64_t hi, const double* x,
-                                          const double* xl, const double* xu, const double* prm, int32_t* cnt,
-                                          int32_t* idx, double* cx, double* cl, double* cu, double* cp) {
-    const int64_t l = lo + blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (l >= hi || !active[l]) return;
-    const int k = atomicAdd(cnt, 1);
-    idx[k] = (int32_t)l;
-    for (int i = 0; i < 6; ++i) {
-        cx[k * 6 + i] = x[l * 6 + i];
-        cl[k * 6 + i] = xl[l * 6 + i];
-        cu[k * 6 + i] = xu[l * 6 + i];
+// ---- line limits: the augmented-Lagrangian loop of every branch, fused.
+// One warp per branch runs its own loop (PAPER.md:271 anticipates an AL kernel
+// on top of TRON): solve the d = 6 subproblem with the current (mu, xi), apply
+// tb_admm_auglag_update, repeat until the branch is feasible or the round cap.
+// Each branch's sequence of solves and updates is exactly the one of the
+// synchronous rounds of the oracle (oracle/admm_oracle.c orc_branch_stage),
+// so results are bit-identical, but a branch never waits for the slowest
+// branch of a round.  x is solved in place (each solve reads x0 before it
+// writes x*).  round_max receives the largest per-branch round count (= the
+// number of synchronous rounds the oracle runs).
+__global__ void __launch_bounds__(32, tbdev::WarpMinBlocks<6>::value)
+    admm_auglag_fused_kernel(const __grid_constant__ tbdev::KernelArgs a, double* prm_shard, double* eta_shard,
+                             double xi0, double eta0, double feas_tol, double xi_max, int max_rounds,
+                             int* round_max) {
+    extern __shared__ double smem[];
+    const long long pid = blockIdx.x;
+    if (pid >= a.count) return;
+    const int lane = threadIdx.x & 31;
+    double* prm = prm_shard + pid * TB_BR_NPARAMS;
+    if (lane == 0) {
+        prm[TB_BR_XI] = xi0;
+        eta_shard[pid] = eta0;
     }
-    for (int i = 0; i < TB_BR_NPARAMS; ++i) cp[k * TB_BR_NPARAMS + i] = prm[l * TB_BR_NPARAMS + i];
+    __syncwarp();
+    int rounds = 0;
+#pragma unroll 1
+    for (int r = 0; r < max_rounds; ++r) {
+        ++rounds;
+        tbdev::tron_solve_one<TB_FAMILY_BRANCH, 6, false>(a, pid, smem);
+        __syncwarp();
+        int active = 0;
+        if (lane == 0) active = tb_admm_auglag_update(a.x_star + pid * 6, prm, eta_shard + pid, feas_tol, xi_max);
+        active = __shfl_sync(0xffffffffu, active, 0);
+        __syncwarp();
+        if (!active) break;
+    }
+    if (lane == 0) atomicMax(round_max, rounds);
 }
 
-// scatter the solutions back and run the AL update of each solved branch
-__global__ void admm_auglag_update_kernel(const int32_t* cnt, const int32_t* idx, const double* cx,
-                                          const int32_t* cst, double* x, int32_t* status, double* prm, double* eta,
-                                          int32_t* active, double feas_tol, double xi_max) {
-    const int k = blockIdx.x * blockDim.x + threadIdx.x;
-    if (k >= *cnt) return;
-    const int64_t l = idx[k];
-    double* xl = x + l * 6;
-    for (int i = 0; i < 6; ++i) xl[i] = cx[k * 6 + i];
-    status[l] = cst[k];
-    active[l] = tb_admm_auglag_update(xl, prm + l * TB_BR_NPARAMS, eta + l, feas_tol, xi_max);
+__global__ void admm_round_accum_kernel(int* round_max, long long* total) {
+    *total += *round_max;
+    *round_max = 0;
 }
 
 __global__ void admm_line_viol_kernel(const double* x, const double* prm, int64_t n, unsigned long long* out) {
@@ -138,12 +144,8 @@ struct tb_admm {
     int dim = 4;
     tb_admm_options opt{};
     double* eta = nullptr;
-    int32_t* active = nullptr;
-    int32_t* cnt = nullptr;
-    int32_t* cidx = nullptr;
-    double *cx = nullptr, *cl = nullptr, *cu = nullptr, *cp = nullptr, *cxo = nullptr;
-    int32_t* cst = nullptr;
-    long long auglag_rounds = 0;
+    int* round_max = nullptr;          // device: largest per-branch round count of this iteration
+    long long* rounds_total = nullptr;  // device: sum over iterations
 };
 
 namespace {
@@ -291,18 +293,12 @@ int tb_admm_create(const tb_admm_grid* gr, const tb_admm_options* opt, int32_t d
         a->res = dalloc<unsigned long long>(a, 2, &err);
         a->cost = dalloc<double>(a, 1, &err);
     }
-    if (err == cudaSuccess && D == 6) {  // AL state + compaction buffers for this shard
-        const size_t m = (size_t)std::max<int64_t>(1, a->br_hi - a->br_lo);
+    if (err == cudaSuccess && D == 6) {  // AL state
         a->eta = dalloc<double>(a, (size_t)nl, &err);
-        a->active = dalloc<int32_t>(a, (size_t)nl, &err);
-        a->cnt = dalloc<int32_t>(a, 1, &err);
-        a->cidx = dalloc<int32_t>(a, m, &err);
-        a->cx = dalloc<double>(a, m * 6, &err);
-        a->cl = dalloc<double>(a, m * 6, &err);
-        a->cu = dalloc<double>(a, m * 6, &err);
-        a->cxo = dalloc<double>(a, m * 6, &err);
-        a->cp = dalloc<double>(a, m * TB_BR_NPARAMS, &err);
-        a->cst = dalloc<int32_t>(a, m, &err);
+        a->round_max = dalloc<int>(a, 1, &err);
+        a->rounds_total = dalloc<long long>(a, 1, &err);
+        if (err == cudaSuccess) err = cudaMemset(a->round_max, 0, sizeof(int));
+        if (err == cudaSuccess) err = cudaMemset(a->rounds_total, 0, sizeof(long long));
     }
     v.br_x = a->x;
     tb_admm_host_free(&hs);
@@ -346,35 +342,27 @@ int tb_admm_solve_components(tb_admm* a, void* stream) {
     }
     const int64_t cnt = a->br_hi - a->br_lo;
     if (cnt > 0 && a->dim == 6) {
-        // augmented-Lagrangian rounds: solve the active branches, update mu / xi
-        const unsigned gb = (unsigned)((cnt + 127) / 128);
-        admm_auglag_reset_kernel<<<gb, 128, 0, st>>>(a->v.br_params, a->eta, a->active, a->br_lo, a->br_hi,
-                                                     a->opt.auglag_xi0, a->opt.auglag_eta0);
-        tbdev::note_launches(1);
-        for (int round = 0; round < a->opt.auglag_max_iter; ++round) {
-            cudaMemsetAsync(a->cnt, 0, sizeof(int32_t), st);
-            admm_auglag_gather_kernel<<<gb, 128, 0, st>>>(a->active, a->br_lo, a->br_hi, a->x, a->lower, a->upper,
-                                                          a->v.br_params, a->cnt, a->cidx, a->cx, a->cl, a->cu,
-                                                          a->cp);
-            tbdev::note_launches(1);
-            int32_t nact = 0;
-            cudaMemcpyAsync(&nact, a->cnt, sizeof nact, cudaMemcpyDeviceToHost, st);
-            const cudaError_t e = cudaStreamSynchronize(st);
-            if (e != cudaSuccess) return fail(TB_E_CUDA, cudaGetErrorString(e));
-            if (nact == 0) break;
-            ++a->auglag_rounds;
-            tb_problem_batch b{TB_FAMILY_BRANCH, 6, nact, a->cx, a->cl, a->cu, a->cp, TB_BR_NPARAMS, TB_MEM_DEVICE};
-            tb_batch_result r{};
-            r.x_star = a->cxo;
-            r.status = a->cst;
-            r.memspace = TB_MEM_DEVICE;
-            const int rc = tb_solve_batch_async(a->ctx, &b, &a->tron, &r, st);
-            if (rc != TB_OK) return fail(rc, tb_last_error());
-            admm_auglag_update_kernel<<<(unsigned)((nact + 127) / 128), 128, 0, st>>>(
-                a->cnt, a->cidx, a->cxo, a->cst, a->x, a->status, a->v.br_params, a->eta, a->active,
-                a->opt.auglag_feas_tol, a->opt.auglag_xi_max);
-            tbdev::note_launches(1);
-        }
+        // the whole augmented-Lagrangian loop of every branch in one launch
+        tbdev::KernelArgs k{};
+        k.n = 6;
+        k.nparams = TB_BR_NPARAMS;
+        k.count = cnt;
+        k.stride = TB_BR_NPARAMS;
+        k.x0 = a->x + a->br_lo * 6;
+        k.lo = a->lower + a->br_lo * 6;
+        k.up = a->upper + a->br_lo * 6;
+        k.prm = a->v.br_params + a->br_lo * TB_BR_NPARAMS;
+        k.cfg = a->tron;
+        k.fast_forward = 1;
+        k.extrap = 1.0 / a->tron.interp_factor;
+        k.x_star = a->x + a->br_lo * 6;  // in place
+        k.status = a->status + a->br_lo;
+        const size_t smem = sizeof(double) * (size_t)(tbdev::SmemLayout<6>::fixed() + TB_BR_NPARAMS);
+        admm_auglag_fused_kernel<<<(unsigned)cnt, 32, smem, st>>>(
+            k, a->v.br_params + a->br_lo * TB_BR_NPARAMS, a->eta + a->br_lo, a->opt.auglag_xi0, a->opt.auglag_eta0,
+            a->opt.auglag_feas_tol, a->opt.auglag_xi_max, a->opt.auglag_max_iter, a->round_max);
+        admm_round_accum_kernel<<<1, 1, 0, st>>>(a->round_max, a->rounds_total);
+        tbdev::note_launches(2);
     } else if (cnt > 0) {
         tb_problem_batch b{TB_FAMILY_BRANCH, 4, cnt, a->x + a->br_lo * 4, a->lower + a->br_lo * 4,
                            a->upper + a->br_lo * 4, a->v.br_params + a->br_lo * TB_BR_NPARAMS, TB_BR_NPARAMS,
@@ -452,9 +440,14 @@ int tb_admm_get(tb_admm* a, int32_t what, void* host_out) {
         case TB_ADMM_BUS_TT: src = v.bus_tt; bytes = sizeof(double) * v.n_bus; break;
         case TB_ADMM_BRANCH_X: src = a->x; bytes = sizeof(double) * a->dim * (size_t)v.n_branch; break;
         case TB_ADMM_AUGLAG_ROUNDS: {
-            const int64_t r = a->auglag_rounds;
-            std::memcpy(host_out, &r, sizeof r);
-            return TB_OK;
+            if (a->dim != 6) {
+                const int64_t z = 0;
+                std::memcpy(host_out, &z, sizeof z);
+                return TB_OK;
+            }
+            src = a->rounds_total;
+            bytes = sizeof(long long);
+            break;
         }
         case TB_ADMM_LINE_VIOL: {
             if (a->dim != 6) return fail(TB_E_INVALID_ARGUMENT, "tb_admm_get: line limits are off");

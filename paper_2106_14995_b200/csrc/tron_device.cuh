@@ -863,13 +863,11 @@ struct WarpMinBlocks {
                                                    : 16;
 };
 
-// tron.hpp:453-549 solve(), one problem per warp (one warp per block).
+// tron.hpp:453-549 solve() of problem `pid` by one warp (the calling warp owns
+// `smem`, SmemLayout<D>::fixed() + params doubles).
 template <int FAM, int D, bool COUNT>
-__global__ void __launch_bounds__(32, WarpMinBlocks<D>::value) tron_solve_kernel(const __grid_constant__ KernelArgs a) {
-    extern __shared__ double smem[];
+__device__ __forceinline__ void tron_solve_one(const KernelArgs& a, const long long pid, double* smem) {
     using SL = SmemLayout<D>;
-    const long long pid = blockIdx.x;
-    if (pid >= a.count) return;
     const unsigned long long t_start = globaltimer();
 
     Warp<D, COUNT> W;
@@ -1052,6 +1050,15 @@ __global__ void __launch_bounds__(32, WarpMinBlocks<D>::value) tron_solve_kernel
         if (a.flops) a.flops[pid] = W.fl;
         if (a.wall_time) a.wall_time[pid] = 1e-9 * (double)(globaltimer() - t_start);
     }
+}
+
+// One problem per warp (one warp per block).
+template <int FAM, int D, bool COUNT>
+__global__ void __launch_bounds__(32, WarpMinBlocks<D>::value) tron_solve_kernel(const __grid_constant__ KernelArgs a) {
+    extern __shared__ double smem[];
+    const long long pid = blockIdx.x;
+    if (pid >= a.count) return;
+    tron_solve_one<FAM, D, COUNT>(a, pid, smem);
 }
 
 }  // namespace tbdev
