@@ -270,3 +270,24 @@ def test_device_admm_line_limits_bitwise_vs_oracle():
     for what in (A.GEN_P, A.GEN_Q, A.BUS_WT, A.BUS_TT, A.BRANCH_X, A.BRANCH_PARAMS, A.BRANCH_STATUS, A.COST,
                  A.AUGLAG_ROUNDS, A.LINE_VIOL):
         assert np.array_equal(dev.get(what), cpu.get(what)), what
+
+
+@pytest.mark.gpu
+def test_sharded_path_world1_line_limits_equals_single():
+    """The torch.distributed driver with the d=6 branch stage (x rows of 6)."""
+    import torch.distributed as dist
+
+    g, _ = _binding_grid()
+    if not dist.is_initialized():
+        import os
+
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ.setdefault("MASTER_PORT", "29534")
+        dist.init_process_group("nccl", rank=0, world_size=1)
+    opts = A.AdmmOptions(line_limits=True)
+    sh = A.ShardedAdmm(g, 0, 1, 0, opts)
+    ref = A.AdmmSolver(g, opts)
+    for k in range(8):
+        assert sh.step() == ref.step(), k
+    assert np.array_equal(sh.solver.get(A.BRANCH_X), ref.get(A.BRANCH_X))
+    assert sh.x.shape[1] == 6
