@@ -121,6 +121,16 @@ def cpu_reference_run(batch, workers, reps=1):
     return best, total
 
 
+def cpu_model() -> str:
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
 def cpu_sample(full_batch, seconds_target=1.5, workers=1, rate_guess=15000.0):
     from paper_2106_14995_b200 import ProblemBatch
 
@@ -457,8 +467,12 @@ def main():
                 sample, n = cpu_sample(batch, seconds_target=2.0, workers=cores)
                 cpu_reference_run(sample, cores)
                 v, _ = cpu_reference_run(sample, cores, reps=3)
+                one, n1 = cpu_sample(batch, seconds_target=1.0, workers=1)
+                v1, _ = cpu_reference_run(one, 1, reps=2)
                 cpu = {"value": v, "unit": "solves/s", "cores": cores, "kind": "reference",
-                       "sample": f"first {n} of the {N} C2 problems, reference solve_batch(workers={cores}), best of 3"}
+                       "sample": f"first {n} of the {N} C2 problems, reference solve_batch(workers={cores}), best of 3",
+                       "cpu_model": cpu_model(), "single_thread_value": v1,
+                       "single_thread_sample": f"first {n1} problems, workers=1, best of 2"}
         except Exception as e:
             cpu = {"value": None, "unit": "solves/s", "cores": None, "kind": "reference", "sample": f"failed: {e}"}
 
