@@ -131,7 +131,8 @@ struct SmemLayout {
     static constexpr int XS = S2 + 2 * D;    // D point for family evaluations
     static constexpr int CTX = XS + D;       // family context (branch: sizeof(tb_branch_ctx))
     static constexpr int CTX_DOUBLES = (int)((sizeof(tb_branch_ctx) / sizeof(double) + 1) & ~1);
-    static constexpr int PRM = CTX + CTX_DOUBLES;  // staged parameters
+    static constexpr int SC = CTX + CTX_DOUBLES;   // 4 warp-uniform loop scalars kept out of registers
+    static constexpr int PRM = SC + 4;             // staged parameters
     static constexpr int fixed() { return PRM; }
     static_assert(D % 2 == 0, "D must be even (16-byte staging loads)");
 };
@@ -851,13 +852,14 @@ __device__ __forceinline__ unsigned long long globaltimer() {
 // latency-bound and its SM throughput grows with resident warps; a few
 // spilled registers cost less than the lost residency).  Measured on B200,
 // device-resident batches: D=6 C2 9.56 / 8.89 / 8.43 / 8.28 /
-// 9.14 ms at 16 / 18 / 22 / 24 / 28; D=4 best at 22, D=8 (masked loops) at
-// 24 (4.00 / 4.58 / 4.49 ms at 24 / 28 / 32), D=16 at 20.
+// 9.14 ms at 16 / 18 / 22 / 24 / 28 before the loop scalars moved to shared
+// memory, 8.22 / 8.09 ms at 24 / 28 after; D=4 best at 22, D=8 (masked
+// loops) at 24 (4.00 / 4.58 / 4.49 ms at 24 / 28 / 32), D=16 at 20.
 template <int D>
 struct WarpMinBlocks {
     static constexpr int value = TB_MIN_BLOCKS > 0 ? TB_MIN_BLOCKS
                                  : D <= 4          ? 22
-                                 : D <= 6          ? 24
+                                 : D <= 6          ? 28
                                  : D <= 8          ? 24
                                  : D <= 16         ? 20
                                                    : 16;
@@ -910,7 +912,7 @@ __device__ __forceinline__ void tron_solve_one(const KernelArgs& a, const long l
 
     int status = TB_STATUS_ITER_LIMIT;
     int iterations = 0;
-    long long cg_iterations = 0, f_evals = 0;
+    long long cg_out = 0, f_evals_out = 0;
     double f = 0.0, pg = 0.0;
 
     // tron.hpp:465-466
@@ -927,7 +929,18 @@ __device__ __forceinline__ void tron_solve_one(const KernelArgs& a, const long l
         double g = 0.0, s = 0.0, delta = 0.0, alpha_c = 1.0;
         bool need_hessian = true;
         long long fl_iter0 = 0, cg_its = 0;
-        double delta_in = 0.0, alpha_in = 0.0;
+        // delta / alpha_c at the start of the iteration (zero-change check) and
+        // the two counters live in shared memory: warp-uniform values read
+        // once per iteration, registers are the residency limit (§4a)
+        double* sc = smem + SL::SC;
+        double& delta_in = sc[0];
+        double& alpha_in = sc[1];
+        long long& cg_iterations = reinterpret_cast<long long*>(sc)[2];
+        long long& f_evals = reinterpret_cast<long long*>(sc)[3];
+        delta_in = 0.0;
+        alpha_in = 0.0;
+        cg_iterations = 0;
+        f_evals = 0;
 #pragma unroll 1
         for (int iter = 0;; ++iter) {
             TB_PH_BEGIN(6)
@@ -1032,6 +1045,8 @@ __device__ __forceinline__ void tron_solve_one(const KernelArgs& a, const long l
             }
             cg_iterations += cg_its;
         }
+        cg_out = cg_iterations;
+        f_evals_out = f_evals;
     }
 
 #ifdef TB_PHASES
@@ -1045,8 +1060,8 @@ __device__ __forceinline__ void tron_solve_one(const KernelArgs& a, const long l
         if (a.pg_norm) a.pg_norm[pid] = pg;
         if (a.status) a.status[pid] = status;
         if (a.iterations) a.iterations[pid] = iterations;
-        if (a.cg_iterations) a.cg_iterations[pid] = cg_iterations;
-        if (a.f_evals) a.f_evals[pid] = f_evals;
+        if (a.cg_iterations) a.cg_iterations[pid] = cg_out;
+        if (a.f_evals) a.f_evals[pid] = f_evals_out;
         if (a.flops) a.flops[pid] = W.fl;
         if (a.wall_time) a.wall_time[pid] = 1e-9 * (double)(globaltimer() - t_start);
     }
