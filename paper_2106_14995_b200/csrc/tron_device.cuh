@@ -131,8 +131,8 @@ struct SmemLayout {
     static constexpr int XS = S2 + 2 * D;    // D point for family evaluations
     static constexpr int CTX = XS + D;       // family context (branch: sizeof(tb_branch_ctx))
     static constexpr int CTX_DOUBLES = (int)((sizeof(tb_branch_ctx) / sizeof(double) + 1) & ~1);
-    static constexpr int SC = CTX + CTX_DOUBLES;   // 4 warp-uniform loop scalars kept out of registers
-    static constexpr int PRM = SC + 4;             // staged parameters
+    static constexpr int SC = CTX + CTX_DOUBLES;   // 8 warp-uniform loop scalars kept out of registers
+    static constexpr int PRM = SC + 8;             // staged parameters
     static constexpr int fixed() { return PRM; }
     static_assert(D % 2 == 0, "D must be even (16-byte staging loads)");
 };
@@ -910,10 +910,23 @@ __device__ __forceinline__ void tron_solve_one(const KernelArgs& a, const long l
     double x = act ? a.x0[pid * n + lane] : 0.0;
     __syncwarp();
 
-    int status = TB_STATUS_ITER_LIMIT;
-    int iterations = 0;
-    long long cg_out = 0, f_evals_out = 0;
-    double f = 0.0, pg = 0.0;
+    // warp-uniform loop state in shared memory (registers are the residency
+    // limit, §4a): every lane stores the same value, reads follow its own store
+    double* sc = smem + SL::SC;
+    double& delta_in = sc[0];  // delta / alpha_c at the start of the iteration (zero-change check)
+    double& alpha_in = sc[1];
+    long long& cg_iterations = reinterpret_cast<long long*>(sc)[2];
+    long long& f_evals = reinterpret_cast<long long*>(sc)[3];
+    double& f = sc[4];
+    double& pg = sc[5];
+    int& iterations = reinterpret_cast<int*>(sc + 6)[0];
+    int& status = reinterpret_cast<int*>(sc + 6)[1];
+    status = TB_STATUS_ITER_LIMIT;
+    iterations = 0;
+    cg_iterations = 0;
+    f_evals = 0;
+    f = 0.0;
+    pg = 0.0;
 
     // tron.hpp:465-466
     if (__any_sync(FULL, act && !(l <= u))) {
@@ -929,18 +942,8 @@ __device__ __forceinline__ void tron_solve_one(const KernelArgs& a, const long l
         double g = 0.0, s = 0.0, delta = 0.0, alpha_c = 1.0;
         bool need_hessian = true;
         long long fl_iter0 = 0, cg_its = 0;
-        // delta / alpha_c at the start of the iteration (zero-change check) and
-        // the two counters live in shared memory: warp-uniform values read
-        // once per iteration, registers are the residency limit (§4a)
-        double* sc = smem + SL::SC;
-        double& delta_in = sc[0];
-        double& alpha_in = sc[1];
-        long long& cg_iterations = reinterpret_cast<long long*>(sc)[2];
-        long long& f_evals = reinterpret_cast<long long*>(sc)[3];
         delta_in = 0.0;
         alpha_in = 0.0;
-        cg_iterations = 0;
-        f_evals = 0;
 #pragma unroll 1
         for (int iter = 0;; ++iter) {
             TB_PH_BEGIN(6)
@@ -1045,8 +1048,6 @@ __device__ __forceinline__ void tron_solve_one(const KernelArgs& a, const long l
             }
             cg_iterations += cg_its;
         }
-        cg_out = cg_iterations;
-        f_evals_out = f_evals;
     }
 
 #ifdef TB_PHASES
@@ -1060,8 +1061,8 @@ __device__ __forceinline__ void tron_solve_one(const KernelArgs& a, const long l
         if (a.pg_norm) a.pg_norm[pid] = pg;
         if (a.status) a.status[pid] = status;
         if (a.iterations) a.iterations[pid] = iterations;
-        if (a.cg_iterations) a.cg_iterations[pid] = cg_out;
-        if (a.f_evals) a.f_evals[pid] = f_evals_out;
+        if (a.cg_iterations) a.cg_iterations[pid] = cg_iterations;
+        if (a.f_evals) a.f_evals[pid] = f_evals;
         if (a.flops) a.flops[pid] = W.fl;
         if (a.wall_time) a.wall_time[pid] = 1e-9 * (double)(globaltimer() - t_start);
     }
