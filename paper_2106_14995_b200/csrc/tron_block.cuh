@@ -54,7 +54,7 @@ struct BlkLayout {
     // nf <= 64, one factor up to nf = 108); larger systems use the block's
     // global fallback slice (LPFULL doubles)
     static constexpr int LPFULL = D * (D + 1) / 2;
-    static constexpr int LP = D >= 128 ? (TB_BLK_MIN128 >= 5 ? 4352 : 5888) : LPFULL;
+    static constexpr int LP = D >= 128 ? (TB_BLK_MIN128 >= 5 ? 4352 : 5856) : LPFULL;
     static constexpr int L = 0;
     static constexpr int RD = L + LP;                // RN(1 / L(p,p))
     static constexpr int S1 = RD + D;                // staging, double buffered
@@ -62,15 +62,15 @@ struct BlkLayout {
     static constexpr int S3 = S2 + 2 * D;
     static constexpr int BB = S3 + 2 * D;            // triangular-solve results
     static constexpr int XS = BB + D;                // evaluation point
-    static constexpr int MISC = XS + D;              // 48 doubles of scalars (BM_*)
-    static constexpr int FIDX = MISC + 48;           // D int32: free index by rank
+    static constexpr int MISC = XS + D;              // 80 doubles of scalars (BM_*)
+    static constexpr int FIDX = MISC + 80;           // D int32: free index by rank
     static constexpr int MSK = FIDX + D / 2;         // 2 x NW uint32 ballot words
     static constexpr int AS = MSK + ((NW + 1) & ~1); // Hessian (ASMEM only)
     static constexpr int total() { return AS + (ASMEM ? D * D : 0); }
     static_assert(LP % 2 == 0, "alignment");
 };
 // MISC slots
-enum { BM_RED = 0, BM_PID = 16, BM_GOK = 18, BM_GFL = 20, BM_GRP = 24, BM_PCG = 40, BM_MISC_SIZE = 48 };
+enum { BM_RED = 0, BM_PID = 16, BM_GOK = 18, BM_GFL = 20, BM_GRP = 24, BM_PCG = 40, BM_SC = 48, BM_MISC_SIZE = 80 };
 
 // a subset of the variables: its size and this thread's ascending rank in it
 // (-1 if absent).  The staged vector of a subset is indexed by rank.
@@ -1076,10 +1076,24 @@ __global__ void __launch_bounds__(D, BlkMinBlocks<D>::value) tron_block_kernel(c
         const double u = act ? a.up[pid * n + t] : 0.0;
         double x = act ? a.x0[pid * n + t] : 0.0;
 
-        int status = TB_STATUS_ITER_LIMIT;
-        int iterations = 0;
-        long long cg_iterations = 0, f_evals = 0;
-        double f = 0.0, pg = 0.0;
+        // block-uniform loop state in shared memory, one copy per warp (warps
+        // run apart between barriers; inside a warp every lane stores the same
+        // value and reads its own store; registers set residency)
+        double* sc = W.misc + BM_SC + 8 * (t >> 5);
+        long long& cg_iterations = reinterpret_cast<long long*>(sc)[0];
+        long long& f_evals = reinterpret_cast<long long*>(sc)[1];
+        double& f = sc[2];
+        double& pg = sc[3];
+        int& iterations = reinterpret_cast<int*>(sc + 4)[0];
+        int& status = reinterpret_cast<int*>(sc + 4)[1];
+        double& delta_in = sc[5];
+        double& alpha_in = sc[6];
+        status = TB_STATUS_ITER_LIMIT;
+        iterations = 0;
+        cg_iterations = 0;
+        f_evals = 0;
+        f = 0.0;
+        pg = 0.0;
 
         if (W.any(act && !(l <= u))) {
             status = TB_STATUS_INVALID_BOUNDS;
@@ -1090,7 +1104,8 @@ __global__ void __launch_bounds__(D, BlkMinBlocks<D>::value) tron_block_kernel(c
             double g = 0.0, s = 0.0, delta = 0.0, alpha_c = 1.0;
             bool need_hessian = true;
             long long fl_iter0 = 0, cg_its = 0;
-            double delta_in = 0.0, alpha_in = 0.0;
+            delta_in = 0.0;
+            alpha_in = 0.0;
 #pragma unroll 1
             for (int iter = 0;; ++iter) {
                 TB_PH_BEGIN(6)
