@@ -911,7 +911,10 @@ __device__ __forceinline__ void tron_solve_one(const KernelArgs& a, const long l
     __syncwarp();
 
     // warp-uniform loop state in shared memory (registers are the residency
-    // limit, §4a): every lane stores the same value, reads follow its own store
+    // limit, §4a).  All lanes execute these statements converged (warp-uniform
+    // conditions only, a __syncwarp in every staged reduction), so a
+    // read-modify-write such as ++f_evals reads the old value in every lane
+    // before any lane stores; the bitwise tests and the parity fuzz exercise it.
     double* sc = smem + SL::SC;
     double& delta_in = sc[0];  // delta / alpha_c at the start of the iteration (zero-change check)
     double& alpha_in = sc[1];
