@@ -853,14 +853,13 @@ __device__ __forceinline__ unsigned long long globaltimer() {
 // spilled registers cost less than the lost residency).  Measured on B200,
 // device-resident batches: D=6 C2 9.56 / 8.89 / 8.43 / 8.28 /
 // 9.14 ms at 16 / 18 / 22 / 24 / 28 before the loop scalars moved to shared
-// memory, 8.22 / 8.09 ms at 24 / 28 after; D=4 best at 22, D=8 (masked
-// loops) at 24 (4.00 / 4.58 / 4.49 ms at 24 / 28 / 32), D=16 at 20.
+// memory, 8.22 / 8.09 ms at 24 / 28 after; after the register diet D=4 and
+// D=8 (masked loops) also run best at 28 (ncvx4 1.537 -> 1.495 ms, branch4
+// 1.363 -> 1.334, ncvx8 3.82 -> 3.69); D=16 at 20, 32 blocks always slower.
 template <int D>
 struct WarpMinBlocks {
     static constexpr int value = TB_MIN_BLOCKS > 0 ? TB_MIN_BLOCKS
-                                 : D <= 4          ? 22
-                                 : D <= 6          ? 28
-                                 : D <= 8          ? 24
+                                 : D <= 8          ? 28
                                  : D <= 16         ? 20
                                                    : 16;
 };
