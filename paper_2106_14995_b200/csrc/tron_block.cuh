@@ -54,7 +54,7 @@ struct BlkLayout {
     // nf <= 64, one factor up to nf = 108); larger systems use the block's
     // global fallback slice (LPFULL doubles)
     static constexpr int LPFULL = D * (D + 1) / 2;
-    static constexpr int LP = D >= 128 ? (TB_BLK_MIN128 >= 5 ? 4352 : 5856) : LPFULL;
+    static constexpr int LP = D >= 128 ? (TB_BLK_MIN128 >= 5 ? 4352 : 5840) : LPFULL;
     static constexpr int L = 0;
     static constexpr int RD = L + LP;                // RN(1 / L(p,p))
     static constexpr int S1 = RD + D;                // staging, double buffered
@@ -62,15 +62,15 @@ struct BlkLayout {
     static constexpr int S3 = S2 + 2 * D;
     static constexpr int BB = S3 + 2 * D;            // triangular-solve results
     static constexpr int XS = BB + D;                // evaluation point
-    static constexpr int MISC = XS + D;              // 80 doubles of scalars (BM_*)
-    static constexpr int FIDX = MISC + 80;           // D int32: free index by rank
+    static constexpr int MISC = XS + D;              // 96 doubles of scalars (BM_*)
+    static constexpr int FIDX = MISC + 96;           // D int32: free index by rank
     static constexpr int MSK = FIDX + D / 2;         // 2 x NW uint32 ballot words
     static constexpr int AS = MSK + ((NW + 1) & ~1); // Hessian (ASMEM only)
     static constexpr int total() { return AS + (ASMEM ? D * D : 0); }
     static_assert(LP % 2 == 0, "alignment");
 };
 // MISC slots
-enum { BM_RED = 0, BM_PID = 16, BM_GOK = 18, BM_GFL = 20, BM_GRP = 24, BM_PCG = 40, BM_SC = 48, BM_MISC_SIZE = 80 };
+enum { BM_RED = 0, BM_PID = 16, BM_GOK = 18, BM_GFL = 22, BM_GRP = 30, BM_PCG = 62, BM_SC = 64, BM_MISC_SIZE = 96 };
 
 // a subset of the variables: its size and this thread's ascending rank in it
 // (-1 if absent).  The staged vector of a subset is indexed by rank.
@@ -354,9 +354,10 @@ struct Blk {
     // independent, so the block splits into G groups of GT threads (GT = 32,
     // 64 or 128 >= nf), each running attempt k0 + g on its own packed factor;
     // the first success in k order is the reference's result.  Groups
-    // synchronise with __syncwarp (GT = 32) or a named barrier.
+    // synchronise with __syncwarp (GT <= 32; two 16-lane groups of a warp step
+    // through the columns in lockstep) or a named barrier.
     __device__ __forceinline__ void gsync(int gid, int gt) {
-        if (gt == 32) __syncwarp();
+        if (gt <= 32) __syncwarp();  // gt = 16: both groups of the warp step in lockstep
         else if (gt == D) __syncthreads();
         else asm volatile("bar.sync %0, %1;" ::"r"(1 + gid), "r"(gt) : "memory");
     }
@@ -365,13 +366,16 @@ struct Blk {
     // group: thread p computes L(p, j) of column j; the division by d of
     // column j is applied at the start of column j + 1 (one barrier per column).
     __device__ __forceinline__ bool chol_attempt(double sh, double* Lg, const double* Bs, double* slot, int p,
-                                                 int gid, int gt, long long& fla) {
+                                                 int gid, int gt, bool valid, long long& fla) {
         const bool rowv = p < nf;
         const double* Ar = A + (rowv ? fidx[p] : 0);
         double* piv = slot;      // [2]
         double* nxt = slot + 2;  // [2]
         double own_prev = 0.0, dprev = 1.0, rprev = 1.0;  // rprev = RN(1 / dprev)
         int csj = 0;                                         // cs(j)
+        // gt = 16: a failed (or never valid) group idles until both groups of
+        // its warp are done; larger groups leave as soon as their pivot fails
+        bool alive = valid;
 #pragma unroll 1
         for (int j = 0; j < nf; ++j) {
             const bool row = rowv && p >= j;
@@ -417,22 +421,29 @@ struct Blk {
             gsync(gid, gt);
             const double pivot = piv[j & 1];
             const bool ok = pivot > 0.0;
-            if (COUNT) fla += 1 + 2LL * (nf - j) * cnt + (ok ? nf - j : 0);
-            if (!ok) return false;
-            const double d = sqrt(pivot);
+            if (COUNT && alive) fla += 1 + 2LL * (nf - j) * cnt + (ok ? nf - j : 0);
+            alive = alive && ok;
+            if (gt > 16) {
+                if (!ok) return false;  // the group is a whole warp or more: uniform exit
+            } else if (!__any_sync(0xffffffffu, alive)) {
+                return false;
+            }
+            const double d = sqrt(alive ? pivot : 1.0);
             if (p == j) Lg[csj] = d;
             own_prev = lij;
             dprev = d;
             rprev = 1.0 / d;
             csj += nf - j;
         }
-        return true;
+        return alive;
     }
 
     // dense.hpp:182-201 shifted_factorize on B.  On success Lw is the factor
     // and RD its reciprocal diagonal.  Returns 0 or FACTORIZATION_FAILED.
     __device__ __forceinline__ int ccf(double& shift) {
-        const int gt = nf <= 32 ? 32 : (nf <= 64 && D > 64 ? 64 : D);
+        // 16-lane groups (4 attempts at once) pay at D = 64 (d = 24: -10 %, d = 64: -3 %);
+        // at D = 128 eight lockstep groups cost more than they save (+2 %)
+        const int gt = (nf <= 16 && D == 64) ? 16 : (nf <= 32 ? 32 : (nf <= 64 && D > 64 ? 64 : D));
         const int G = D / gt;
         const int gid = t / gt, p = t % gt;
         const int lpg = ((nf * (nf + 1)) / 2 + 1) & ~1;
@@ -469,9 +480,9 @@ struct Blk {
             const bool valid = (k0 + gid == 0) || (sh <= cap);
             long long fla = 0;
             bool ok = false;
-            if (valid) {
+            if (valid || gt == 16) {  // 16-lane groups share a warp: both enter the lockstep loop
                 TB_PH_BEGIN(11)
-                ok = chol_attempt(sh, Lg, Bs, misc + BM_GRP + 4 * gid, p, gid, gt, fla);
+                ok = chol_attempt(sh, Lg, Bs, misc + BM_GRP + 4 * gid, p, gid, gt, valid, fla);
                 TB_PH_END(*this, 11)
             }
             if (p == 0) {
