@@ -40,6 +40,9 @@
 #ifndef TB_BLK_MIN128
 #define TB_BLK_MIN128 4  // resident D = 128 blocks per SM (registers / shared factor region)
 #endif
+#ifndef TB_BLK_MIN32
+#define TB_BLK_MIN32 16  // D = 32: one warp per problem
+#endif
 #ifndef TB_BLK_MIN64
 #define TB_BLK_MIN64 8
 #endif
@@ -57,10 +60,11 @@ struct BlkLayout {
     static constexpr int LP = D >= 128 ? (TB_BLK_MIN128 >= 5 ? 4352 : 5840) : LPFULL;
     static constexpr int L = 0;
     static constexpr int RD = L + LP;                // RN(1 / L(p,p))
+    static constexpr int SW = 2 * D < 128 ? 128 : 2 * D;  // staging width (warp PCG uses 128)
     static constexpr int S1 = RD + D;                // staging, double buffered
-    static constexpr int S2 = S1 + 2 * D;
-    static constexpr int S3 = S2 + 2 * D;
-    static constexpr int BB = S3 + 2 * D;            // triangular-solve results
+    static constexpr int S2 = S1 + SW;
+    static constexpr int S3 = S2 + SW;
+    static constexpr int BB = S3 + SW;               // triangular-solve results
     static constexpr int XS = BB + D;                // evaluation point
     static constexpr int MISC = XS + D;              // 96 doubles of scalars (BM_*)
     static constexpr int FIDX = MISC + 96;           // D int32: free index by rank
@@ -423,7 +427,7 @@ struct Blk {
             const bool ok = pivot > 0.0;
             if (COUNT && alive) fla += 1 + 2LL * (nf - j) * cnt + (ok ? nf - j : 0);
             alive = alive && ok;
-            if (gt > 16) {
+            if (gt >= 32) {
                 if (!ok) return false;  // the group is a whole warp or more: uniform exit
             } else if (!__any_sync(0xffffffffu, alive)) {
                 return false;
@@ -443,7 +447,9 @@ struct Blk {
     __device__ __forceinline__ int ccf(double& shift) {
         // 16-lane groups (4 attempts at once) pay at D = 64 (d = 24: -10 %, d = 64: -3 %);
         // at D = 128 eight lockstep groups cost more than they save (+2 %)
-        const int gt = (nf <= 16 && D == 64) ? 16 : (nf <= 32 ? 32 : (nf <= 64 && D > 64 ? 64 : D));
+        const int gt = (D == 32 && nf <= 8)    ? 8
+                       : (nf <= 16 && D <= 64) ? 16
+                       : (nf <= 32 ? 32 : (nf <= 64 && D > 64 ? 64 : D));
         const int G = D / gt;
         const int gid = t / gt, p = t % gt;
         const int lpg = ((nf * (nf + 1)) / 2 + 1) & ~1;
@@ -480,7 +486,7 @@ struct Blk {
             const bool valid = (k0 + gid == 0) || (sh <= cap);
             long long fla = 0;
             bool ok = false;
-            if (valid || gt == 16) {  // 16-lane groups share a warp: both enter the lockstep loop
+            if (valid || gt < 32) {  // sub-warp groups share a warp: all enter the lockstep loop
                 TB_PH_BEGIN(11)
                 ok = chol_attempt(sh, Lg, Bs, misc + BM_GRP + 4 * gid, p, gid, gt, valid, fla);
                 TB_PH_END(*this, 11)
@@ -1023,7 +1029,7 @@ struct BlkFamily {
 constexpr size_t kBlkWsHeader = 256;
 template <int D>
 struct BlkMinBlocks {
-    static constexpr int value = D >= 128 ? TB_BLK_MIN128 : TB_BLK_MIN64;
+    static constexpr int value = D >= 128 ? TB_BLK_MIN128 : (D >= 64 ? TB_BLK_MIN64 : TB_BLK_MIN32);
 };
 // ws = header | A slices (grid x D^2, global-A variant) | factor fallback
 // slices (grid x LPFULL, D = 128 only)

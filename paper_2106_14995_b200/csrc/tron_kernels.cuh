@@ -40,15 +40,22 @@ inline bool blk_asmem() {
     return e && e[0] == '1';
 }
 
-// smallest dimension routed to the block kernel: 21 (measured crossover on
-// ncvx, B = 32,768: d = 17 / 20 equal, d = 24 / 28 / 32 1.12x / 1.15x / 1.27x
-// faster on the D = 64 block kernel, whose compacted free systems allow two
-// parallel shift attempts where the D = 32 warp kernel runs one).  Override
-// with TB_BLOCK_MIN_DIM (17..33) for experiments.
+// Dimension routing (ncvx, B = 32,768, device-resident, ms):
+//   d        12     16     17..20        24     32
+//   warp    8.65  11.41  24.4 / 27.4     -      -     (D = 16 / 32 warp kernel)
+//   blk32  10.96  14.47  ~/ 20.19      25.98  48.21   (one-warp block kernel)
+//   blk64  14.85  19.28  ~/ 25.22      30.19  50.10
+// so d <= 16 runs the warp kernel, 17..32 the one-warp D = 32 block kernel
+// (compacted systems, 8/16-lane lockstep attempt groups), 33..64 D = 64 and
+// 65..128 D = 128.  TB_BLOCK_MIN_DIM (9..33) and TB_BLOCK32=0 override.
 inline int blk_min_dim() {
     const char* e = std::getenv("TB_BLOCK_MIN_DIM");
-    const int v = e ? std::atoi(e) : 21;
-    return v < 17 ? 17 : v;
+    const int v = e ? std::atoi(e) : 17;
+    return v < 9 ? 9 : v;
+}
+inline bool blk32() {
+    const char* e = std::getenv("TB_BLOCK32");
+    return !(e && e[0] == '0');
 }
 
 // persistent grid: resident blocks per SM x SMs, capped by the batch
