@@ -132,7 +132,7 @@ int tb_context_set_mode(tb_context* ctx, int32_t mode, int32_t fast_forward);
 /* solve_batch (batch.hpp:27-78): blocking.  Returns TB_E_PROBLEM if any
  * problem reports a status >= TB_STATUS_EVALUATION_ERROR (the reference would
  * have thrown); results are still written.  Dimensions 1..128: one warp per
- * problem up to d = 20, a block of 64 / 128 threads per problem above
+ * problem up to d = 16, a block of 32 / 64 / 128 threads per problem above
  * (persistent grid, workspace owned by the context); larger d is rejected with
  * TB_E_INVALID_ARGUMENT. */
 int tb_solve_batch(tb_context* ctx, const tb_problem_batch* batch, const tb_tron_config* cfg,
