@@ -208,9 +208,9 @@ def test_dimension_over_device_capacity_rejected(solver):
 
 # ------------------------------------------------- d > 32: the block kernel
 @pytest.mark.parametrize("asmem", ["0", "1"])
-@pytest.mark.parametrize("d", [33, 40, 64, 65, 100, 128])
+@pytest.mark.parametrize("d", [17, 24, 32, 33, 40, 64, 65, 100, 128])
 def test_block_kernel_ncvx_bitwise(solver, monkeypatch, d, asmem):
-    """C3 sweep past one warp: D = 64 / 128 threads per problem, Hessian in
+    """C3 sweep on the block kernel: D = 32 / 64 / 128 threads per problem, Hessian in
     the global workspace (default) or in shared memory (TB_BLOCK_ASMEM=1);
     every field, and the flop counters, bit-identical to the oracle."""
     monkeypatch.setenv("TB_BLOCK_ASMEM", asmem)
