@@ -118,6 +118,16 @@ __global__ void admm_line_viol_kernel(const double* x, const double* prm, int64_
 
 thread_local std::string g_admm_err;
 
+// selects `dev` for the scope of an entry point and restores the caller's device
+struct DeviceGuard {
+    int prev = 0;
+    explicit DeviceGuard(int dev) {
+        cudaGetDevice(&prev);
+        cudaSetDevice(dev);
+    }
+    ~DeviceGuard() { cudaSetDevice(prev); }
+};
+
 int fail(int code, const std::string& m) {
     g_admm_err = m;
     return code;
@@ -140,6 +150,7 @@ struct tb_admm {
     int bus_lo = 0, bus_hi = 0;
     tb_tron_config tron{};
     long long iterations = 0;
+    cudaStream_t last = nullptr;  // stream of the latest enqueued stage (tb_admm_get waits for it)
     // line limits (dim 6)
     int dim = 4;
     tb_admm_options opt{};
@@ -334,8 +345,9 @@ int tb_admm_destroy(tb_admm* a) {
 // `stream` (NULL: the ADMM's own stream); returns without synchronising.
 int tb_admm_solve_components(tb_admm* a, void* stream) {
     if (!a) return fail(TB_E_INVALID_ARGUMENT, "null admm");
-    cudaSetDevice(a->device);
+    DeviceGuard guard(a->device);
     cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : a->stream;
+    a->last = st;
     if (a->v.n_gen > 0) {
         admm_gen_kernel<<<(a->v.n_gen + 127) / 128, 128, 0, st>>>(a->v);
         tbdev::note_launches(1);
@@ -393,8 +405,9 @@ int tb_admm_branch_solution(tb_admm* a, double** x_dev, int64_t* lo, int64_t* hi
 // non-NULL; enqueued on `stream`.
 int tb_admm_update_consensus(tb_admm* a, void* stream, double* res2_dev) {
     if (!a) return fail(TB_E_INVALID_ARGUMENT, "null admm");
-    cudaSetDevice(a->device);
+    DeviceGuard guard(a->device);
     cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : a->stream;
+    a->last = st;
     cudaMemsetAsync(a->res, 0, 2 * sizeof(unsigned long long), st);
     // 32-thread blocks: one bus per thread with serial per-bus work, spread over every SM
     admm_bus_kernel<<<(a->v.n_bus + 31) / 32, 32, 0, st>>>(a->v, a->bus_lo, a->bus_hi, a->res);
@@ -408,6 +421,8 @@ int tb_admm_update_consensus(tb_admm* a, void* stream, double* res2_dev) {
 // one full iteration in a single process (no exchange needed), blocking;
 // primal / dual residuals to host
 int tb_admm_step(tb_admm* a, double* primal, double* dual) {
+    if (!a) return fail(TB_E_INVALID_ARGUMENT, "null admm");
+    DeviceGuard guard(a->device);
     int rc = tb_admm_solve_components(a, nullptr);
     if (rc) return rc;
     rc = tb_admm_update_consensus(a, nullptr, nullptr);
@@ -424,7 +439,8 @@ int tb_admm_step(tb_admm* a, double* primal, double* dual) {
 // copy a state array to host: what = TB_ADMM_*
 int tb_admm_get(tb_admm* a, int32_t what, void* host_out) {
     if (!a || !host_out) return fail(TB_E_INVALID_ARGUMENT, "null argument");
-    cudaSetDevice(a->device);
+    DeviceGuard guard(a->device);
+    if (a->last && a->last != a->stream) cudaStreamSynchronize(a->last);  // stages enqueued on a caller stream
     cudaStreamSynchronize(a->stream);
     const tb_admm_view& v = a->v;
     const void* src = nullptr;

@@ -405,7 +405,13 @@ extern "C" int tb_solve_batch_async(tb_context* ctx, const tb_problem_batch* b, 
     if (ctx->devs.size() != 1 || b->memspace != TB_MEM_DEVICE || r->memspace != TB_MEM_DEVICE)
         return set_err(TB_E_INVALID_ARGUMENT, "solve_batch_async: needs a 1-device context and device memory");
     DevState& d = ctx->devs[0];
+    int prev = 0;
+    cudaGetDevice(&prev);
     CUDA_TRY(cudaSetDevice(d.device));
+    struct Restore {
+        int dev;
+        ~Restore() { cudaSetDevice(dev); }
+    } restore{prev};  // the caller's current device is left as it was
     cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : d.stream;
     OutPtrs o{r->x_star, r->f_star, r->pg_norm, r->status, r->iterations, r->cg_iterations, r->f_evals, r->flops,
               r->wall_time};

@@ -291,3 +291,24 @@ def test_sharded_path_world1_line_limits_equals_single():
         assert sh.step() == ref.step(), k
     assert np.array_equal(sh.solver.get(A.BRANCH_X), ref.get(A.BRANCH_X))
     assert sh.x.shape[1] == 6
+
+
+@pytest.mark.gpu
+def test_get_after_stages_on_caller_stream_sees_their_results():
+    """tb_admm_get waits for the caller stream the stages were enqueued on (no
+    host sync in between), and the entry points leave the current device alone."""
+    import torch
+
+    g = synth.grid(400, 560, 120, seed=5)
+    dev = A.AdmmSolver(g)
+    ref = A.AdmmSolver(g)
+    s = torch.cuda.Stream()
+    before = torch.cuda.current_device()
+    for k in range(4):
+        ref.step()
+        dev.solve_components(s.cuda_stream)
+        dev.update_consensus(s.cuda_stream)
+        # no synchronisation here: get must order itself after stream s
+        assert np.array_equal(dev.get(A.BRANCH_X), ref.get(A.BRANCH_X)), k
+        assert np.array_equal(dev.get(A.BUS_WT), ref.get(A.BUS_WT)), k
+    assert torch.cuda.current_device() == before
