@@ -525,14 +525,18 @@ struct Blk {
         }
     }
 
-    // forward solve L b = rhs in compacted ownership (column sweep)
-    __device__ __forceinline__ double trsv_fwd(double b) {
+    // forward solve L b = rhs in compacted ownership (column sweep).  The
+    // quotients take the branch-free Markstein form (tron_device.cuh `quot`);
+    // one barrier-vote at the end sends a solve that met an out-of-range
+    // quotient through the IEEE divisions again (same results as div_rcp).
+    template <bool IEEE>
+    __device__ __forceinline__ double trsv_fwd_core(double b, bool& bad) {
         const int p = t;
         double s = p < nf ? b : 0.0;
 #pragma unroll 1
         for (int j = 0; j < nf; ++j) {
             if (p == j) {
-                s = div_rcp(s, Lat(j, j), RD[j]);
+                s = quot<IEEE>(s, Lat(j, j), RD[j], bad);
                 bb[j] = s;
             }
             sync();
@@ -540,6 +544,12 @@ struct Blk {
             if (p > j && p < nf) s -= Lat(p, j) * q;
         }
         return s;
+    }
+    __device__ __forceinline__ double trsv_fwd(double b) {
+        bool bad = false;
+        const double s = trsv_fwd_core<false>(b, bad);
+        if (!__syncthreads_or(bad)) return s;
+        return trsv_fwd_core<true>(b, bad);
     }
     // backward solve L^T b = rhs (dense.hpp:229-235): for i descending,
     // s = b_i - sum_{j > i ascending} L(j,i) b_j, serial on warp 0 (all lanes
@@ -549,13 +559,19 @@ struct Blk {
         tog ^= D;
         if (t < nf) in[t] = b;
         sync();
-        if (t < 32) bwd_core(in);
+        if (t < 32) bwd_solve(in);
         sync();
         return t < nf ? bb[t] : 0.0;
     }
     // the serial backward recurrence, run by warp 0 (lanes compute the same
-    // values); results in bb[0..nf-1]
-    __device__ __forceinline__ void bwd_core(const double* in) {
+    // values, so `bad` is warp-uniform); results in bb[0..nf-1]
+    __device__ __forceinline__ void bwd_solve(const double* in) {
+        bool bad = false;
+        bwd_core<false>(in, bad);
+        if (bad) bwd_core<true>(in, bad);
+    }
+    template <bool IEEE>
+    __device__ __forceinline__ void bwd_core(const double* in, bool& bad) {
         double last = 0.0;
 #pragma unroll 1
         for (int i = nf - 1; i >= 0; --i) {
@@ -576,7 +592,7 @@ struct Blk {
             }
 #pragma unroll 1
             for (; j < nf; ++j) s -= Lc[j] * bb[j];
-            last = div_rcp(s, Lc[i], RD[i]);
+            last = quot<IEEE>(s, Lc[i], RD[i], bad);
             if (t == 0) bb[i] = last;
             __syncwarp();
         }
@@ -614,23 +630,29 @@ struct Blk {
         count(2 * nf);
         return wsum(x * y);
     }
-    __device__ __forceinline__ double wtrsv_fwd(double b) {
+    template <bool IEEE>
+    __device__ __forceinline__ double wtrsv_fwd_core(double b, bool& bad) {
         const int p = t;
         double s = p < nf ? b : 0.0;
 #pragma unroll 1
         for (int j = 0; j < nf; ++j) {
-            const double q = div_rcp(__shfl_sync(FULL, s, j), Lat(j, j), RD[j]);
+            const double q = quot<IEEE>(__shfl_sync(FULL, s, j), Lat(j, j), RD[j], bad);
             if (p == j) s = q;
             else if (p > j && p < nf) s -= Lat(p, j) * q;
         }
         return s;
+    }
+    __device__ __forceinline__ double wtrsv_fwd(double b) {  // warp 0; `bad` is warp-uniform
+        bool bad = false;
+        const double s = wtrsv_fwd_core<false>(b, bad);
+        return bad ? wtrsv_fwd_core<true>(b, bad) : s;
     }
     __device__ __forceinline__ double wtrsv_bwd(double b) {
         double* in = s2 + 64 + wtog;
         wtog ^= 32;
         if (t < nf) in[t] = b;
         __syncwarp();
-        bwd_core(in);
+        bwd_solve(in);
         return t < nf ? bb[t] : 0.0;
     }
     __device__ __forceinline__ double wgemv_c(double z) {

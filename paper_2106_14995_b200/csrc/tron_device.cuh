@@ -137,6 +137,10 @@ struct SmemLayout {
     static_assert(D % 2 == 0, "D must be even (16-byte staging loads)");
 };
 
+#ifndef TB_FWD_REDUNDANT
+#define TB_FWD_REDUNDANT 0
+#endif
+
 // ------------------------------------------------------------ solves
 // Correctly rounded a / d from r = RN(1/d) (Markstein): q0 = RN(a r),
 // e = a - d q0 exactly (FMA), RN(q0 + e r) == RN(a / d) when no intermediate
@@ -150,16 +154,54 @@ __device__ __forceinline__ double div_rcp(double a, double d, double r) {
     return fma(e, r, q0);
 }
 
+// The same quotient without the branch: the range test only sets `bad`.  A
+// branch on a value computed from the quotient stalls the warp until the
+// test resolves (~100 cycles per quotient in a dependent chain, measured:
+// scripts/micro/latency.cu), so the triangular solves run every quotient
+// through this form and test `bad` once at the end; a solve that met an
+// out-of-range quotient is recomputed with IEEE divisions (identical results
+// to div_rcp everywhere).
+template <bool IEEE>
+__device__ __forceinline__ double quot(double a, double d, double r, bool& bad) {
+    if (IEEE) return a / d;
+    const double q0 = a * r;
+    const unsigned ex = ((unsigned)__double2hiint(q0) >> 20) & 0x7FFu;
+    bad |= ex - 64u > 1918u;
+    const double e = fma(-q0, d, a);
+    return fma(e, r, q0);
+}
+
 // dense.hpp:224-228 forward solve L b = rhs on F (column sweep == the
 // reference's ascending row dot-form, element by element); lane j's value is
 // broadcast and every lane divides it (uniform operands, no divergence).
-template <int D, bool UNROLL>
-__device__ TB_SOLVE_INLINE double trsv_fwd_fn(const double* __restrict__ Lw, const double* __restrict__ RD, double b,
-                                             unsigned F, int lane) {
+// Fully unrolled builds run the row dot-form redundantly on every lane instead
+// (the right-hand side gathered once up front; identical bits on all lanes).
+template <int D, bool UNROLL, bool IEEE>
+__device__ __forceinline__ double trsv_fwd_core(const double* __restrict__ Lw, const double* __restrict__ RD, double b,
+                                                unsigned F, int lane, bool& bad) {
     const bool inF = lane < D && in_mask(F, lane);
+#if TB_FWD_REDUNDANT
+    if (UNROLL) {
+        double bv[D];
+#pragma unroll
+        for (int j = 0; j < D; ++j) bv[j] = __shfl_sync(FULL, b, j);
+        double out = 0.0;
+#pragma unroll
+        for (int i = 0; i < D; ++i) {
+            if (!in_mask(F, i)) continue;
+            double s = bv[i];
+#pragma unroll
+            for (int j = 0; j < i; ++j)
+                if (in_mask(F, j)) s -= Lw[i + j * D] * bv[j];
+            bv[i] = quot<IEEE>(s, Lw[i + i * D], RD[i], bad);
+            if (lane == i) out = bv[i];
+        }
+        return out;
+    }
+#endif
     double s = inF ? b : 0.0;
     auto step = [&](int j) {
-        const double q = div_rcp(__shfl_sync(FULL, s, j), Lw[j + j * D], RD[j]);
+        const double q = quot<IEEE>(__shfl_sync(FULL, s, j), Lw[j + j * D], RD[j], bad);
         if (lane == j) s = q;
         else if (inF && lane > j) s -= Lw[lane + j * D] * q;
     };
@@ -177,9 +219,9 @@ __device__ TB_SOLVE_INLINE double trsv_fwd_fn(const double* __restrict__ Lw, con
 // dense.hpp:229-235 backward solve L^T b = rhs on F, exact order: for i
 // descending, s = b_i - sum_{j > i ascending} L(j,i) b_j.  Every lane computes
 // every b_i (redundantly, identical bits); bb is D doubles of staging.
-template <int D, bool UNROLL>
-__device__ TB_SOLVE_INLINE double trsv_bwd_fn(const double* __restrict__ Lw, const double* __restrict__ RD,
-                                             double* __restrict__ bb, double b, unsigned F, int lane) {
+template <int D, bool UNROLL, bool IEEE>
+__device__ __forceinline__ double trsv_bwd_core(const double* __restrict__ Lw, const double* __restrict__ RD,
+                                                double* __restrict__ bb, double b, unsigned F, int lane, bool& bad) {
     double out = b;
     if (UNROLL) {
         double bv[D];
@@ -191,7 +233,7 @@ __device__ TB_SOLVE_INLINE double trsv_bwd_fn(const double* __restrict__ Lw, con
 #pragma unroll
             for (int j = i + 1; j < D; ++j)
                 if (in_mask(F, j)) s -= Lw[j + i * D] * bv[j];
-            bv[i] = div_rcp(s, Lw[i + i * D], RD[i]);
+            bv[i] = quot<IEEE>(s, Lw[i + i * D], RD[i], bad);
             if (lane == i) out = bv[i];
         }
     } else {
@@ -204,7 +246,7 @@ __device__ TB_SOLVE_INLINE double trsv_bwd_fn(const double* __restrict__ Lw, con
                 const int j = low_bit(mj);
                 s -= Lw[j + i * D] * bb[j];
             }
-            const double bi = div_rcp(s, Lw[i + i * D], RD[i]);
+            const double bi = quot<IEEE>(s, Lw[i + i * D], RD[i], bad);
             if (lane == i) {
                 out = bi;
                 bb[i] = bi;
@@ -213,6 +255,35 @@ __device__ TB_SOLVE_INLINE double trsv_bwd_fn(const double* __restrict__ Lw, con
         }
     }
     return out;
+}
+
+// the rare recomputation with IEEE divisions, out of line
+template <int D, bool UNROLL>
+__device__ __noinline__ double trsv_fwd_ieee(const double* Lw, const double* RD, double b, unsigned F, int lane) {
+    bool bad = false;
+    return trsv_fwd_core<D, UNROLL, true>(Lw, RD, b, F, lane, bad);
+}
+template <int D, bool UNROLL>
+__device__ __noinline__ double trsv_bwd_ieee(const double* Lw, const double* RD, double* bb, double b, unsigned F,
+                                             int lane) {
+    bool bad = false;
+    return trsv_bwd_core<D, UNROLL, true>(Lw, RD, bb, b, F, lane, bad);
+}
+
+// `bad` is warp-uniform: every lane forms every quotient from the same operands
+template <int D, bool UNROLL>
+__device__ TB_SOLVE_INLINE double trsv_fwd_fn(const double* __restrict__ Lw, const double* __restrict__ RD, double b,
+                                             unsigned F, int lane) {
+    bool bad = false;
+    const double out = trsv_fwd_core<D, UNROLL, false>(Lw, RD, b, F, lane, bad);
+    return bad ? trsv_fwd_ieee<D, UNROLL>(Lw, RD, b, F, lane) : out;
+}
+template <int D, bool UNROLL>
+__device__ TB_SOLVE_INLINE double trsv_bwd_fn(const double* __restrict__ Lw, const double* __restrict__ RD,
+                                             double* __restrict__ bb, double b, unsigned F, int lane) {
+    bool bad = false;
+    const double out = trsv_bwd_core<D, UNROLL, false>(Lw, RD, bb, b, F, lane, bad);
+    return bad ? trsv_bwd_ieee<D, UNROLL>(Lw, RD, bb, b, F, lane) : out;
 }
 
 // ---------------------------------------------------------------- per warp
