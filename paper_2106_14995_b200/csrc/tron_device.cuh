@@ -502,10 +502,15 @@ struct Warp {
             --rem;
             __syncwarp();
         };
+        // Unrolled (D <= 6): every column of F, without a per-column vote on
+        // the groups' pivots -- a vote + branch in the column chain costs more
+        // than the columns a round whose attempts all fail early would skip
+        // (dead groups neither store nor count).  Masked loops (D >= 8, where
+        // failing rounds are long) stop once every group has failed.
         if (kUnroll) {
 #pragma unroll
             for (int j = 0; j < D; ++j)
-                if (in_mask(F, j) && __any_sync(FULL, alive)) column(j);
+                if (in_mask(F, j)) column(j);
         } else {
 #pragma unroll 1
             for (unsigned mj = F; mj && __any_sync(FULL, alive); mj &= mj - 1) column(low_bit(mj));
