@@ -122,6 +122,12 @@ def solve_batch(batch, x0=None, cfg=None, workers=1, impl="oracle") -> Result:
     c = config_c(cfg)
     wall = C.c_double()
     if impl == "oracle":
+        # solve() validates first (tron.hpp:457 -> :70-80, std::invalid_argument)
+        v = oracle_lib().fn("config_validate")
+        v.restype = C.c_int
+        msg = C.c_char_p()
+        if v(C.byref(c), C.byref(msg)):
+            raise ValueError(msg.value.decode())
         f = oracle_lib().fn("solve_batch")
         f.restype = C.c_int
         r.rc = f(int(batch.family), n, C.c_int64(N), _p(x0), _p(lo), _p(up), _p(prm), C.c_int64(stride),

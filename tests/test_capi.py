@@ -47,6 +47,22 @@ def test_validate_uses_reference_messages():
         TronConfig(max_iter=0).validate()
 
 
+@pytest.mark.parametrize("bad", [dict(tol_pg=0.0), dict(delta0=-1.0), dict(eta0=1.0), dict(mu0=0.0),
+                                 dict(interp_factor=1.0), dict(max_iter=0), dict(sigma1=0.6)])
+def test_oracle_and_product_reject_the_same_configs(bad):
+    """The oracle's solve_batch validates first like solve() (tron.hpp:457),
+    with the messages the product raises (tb_config_validate)."""
+    from oracle import pyoracle as po
+    from paper_2106_14995_b200 import synth
+
+    cfg = TronConfig(**bad)
+    with pytest.raises(ValueError) as prod:
+        cfg.validate()
+    with pytest.raises(ValueError) as orc:
+        po.solve_batch(synth.boxqp(2, 3), cfg=cfg, impl="oracle")
+    assert str(orc.value) == str(prod.value)
+
+
 def test_family_nparams():
     assert family_nparams(0, 8) == 0
     assert family_nparams(1, 4) == 20

@@ -342,3 +342,28 @@ def test_block_kernel_large_free_systems_use_global_factor_slice(solver, d):
         ref = po.solve_batch(b, impl="oracle", workers=6)
         assert_bitwise(res, ref, label=f"wide bounds d={d} fam={b.family}")
         assert np.array_equal(host(res.flops), ref.flops)
+
+
+@pytest.mark.parametrize("d", [4, 6, 8, 16, 24, 40])
+@pytest.mark.parametrize("h_scale,c_scale,x_scale", [(1e-200, 1e200, 1e300), (1e-300, 1.0, 1.0), (1.0, 1.0, 1.0)])
+def test_extreme_scales_take_the_ieee_division_path(solver, d, h_scale, c_scale, x_scale):
+    """Box QPs scaled so the triangular-solve quotients leave the Markstein
+    range (|q| > 2^958): H ~ 1e-200 with gradients ~ 1e200 (forward-solve
+    quotients ~ 1e300), H ~ 1e-300 with gradients ~ 1 (backward-solve
+    quotients ~ 1e300); both reach the PCG in the oracle.  The branch-free
+    quotients flag it and the solve is recomputed with IEEE divisions
+    (DESIGN.md §3).  Warp (d <= 16) and block (d = 24, 40) kernels, bitwise
+    against the oracle; unscaled control case."""
+    from paper_2106_14995_b200 import ProblemBatch
+
+    b = synth.boxqp(48, d, seed=40 + d)
+    params = b.params.copy()
+    params[:, :d * d] *= h_scale
+    params[:, d * d:] *= c_scale
+    sb = ProblemBatch(b.family, d, b.lower * x_scale, b.upper * x_scale, np.ascontiguousarray(params),
+                      b.x0 * x_scale)
+    cfg = TronConfig(max_iter=25, tol_pg=1e-300)
+    res = solver.solve_batch(sb, cfg=cfg, count_flops=True)
+    ref = po.solve_batch(sb, cfg=cfg, impl="oracle", workers=8)
+    assert_bitwise(res, ref, label=f"d={d} h={h_scale} c={c_scale}")
+    assert np.array_equal(host(res.flops), ref.flops)
