@@ -369,8 +369,12 @@ struct Blk {
     // cholesky_left_looking (dense.hpp:138-156) on B = A[F,F] + sh I by one
     // group: thread p computes L(p, j) of column j; the division by d of
     // column j is applied at the start of column j + 1 (one barrier per column).
+    // The quotients are branch-free (`quot`, tron_device.cuh); `bad` reports
+    // one that left the Markstein range and ccf reruns the round with IEEE
+    // divisions (IEEE = true).
+    template <bool IEEE>
     __device__ __forceinline__ bool chol_attempt(double sh, double* Lg, const double* Bs, double* slot, int p,
-                                                 int gid, int gt, bool valid, long long& fla) {
+                                                 int gid, int gt, bool valid, long long& fla, bool& bad) {
         const bool rowv = p < nf;
         const double* Ar = A + (rowv ? fidx[p] : 0);
         double* piv = slot;      // [2]
@@ -410,9 +414,9 @@ struct Blk {
             // term k = j-1: L(j, j-1) and L(p, j-1) are the quotients of the
             // raw values by d_{j-1} (IEEE, via the correctly rounded reciprocal)
             if (j > 0) {
-                const double ljprev = div_rcp(nxt[(j - 1) & 1], dprev, rprev);
+                const double ljprev = quot<IEEE>(nxt[(j - 1) & 1], dprev, rprev, bad);
                 if (row) {
-                    own_prev = div_rcp(own_prev, dprev, rprev);
+                    own_prev = quot<IEEE>(own_prev, dprev, rprev, bad);
                     Lg[c + p] = own_prev;  // c == cs(j-1) - (j-1)
                 }
                 if (ljprev != 0.0) {
@@ -436,7 +440,7 @@ struct Blk {
             if (p == j) Lg[csj] = d;
             own_prev = lij;
             dprev = d;
-            rprev = 1.0 / d;
+            rprev = __drcp_rn(d);  // RN(1/d), the same bits as 1.0 / d
             csj += nf - j;
         }
         return alive;
@@ -485,11 +489,17 @@ struct Blk {
             for (int q = 0; q < gid; ++q) sh = tb_smax(2.0 * sh, alpha0);
             const bool valid = (k0 + gid == 0) || (sh <= cap);
             long long fla = 0;
-            bool ok = false;
+            bool ok = false, bad = false;
             if (valid || gt < 32) {  // sub-warp groups share a warp: all enter the lockstep loop
                 TB_PH_BEGIN(11)
-                ok = chol_attempt(sh, Lg, Bs, misc + BM_GRP + 4 * gid, p, gid, gt, valid, fla);
+                ok = chol_attempt<false>(sh, Lg, Bs, misc + BM_GRP + 4 * gid, p, gid, gt, valid, fla, bad);
                 TB_PH_END(*this, 11)
+            }
+            if (__syncthreads_or(bad)) {  // rare: rerun the round with IEEE divisions
+                fla = 0;
+                ok = false;
+                if (valid || gt < 32)
+                    ok = chol_attempt<true>(sh, Lg, Bs, misc + BM_GRP + 4 * gid, p, gid, gt, valid, fla, bad);
             }
             if (p == 0) {
                 gok[gid] = ok ? 1 : (valid ? 0 : -1);
@@ -513,7 +523,7 @@ struct Blk {
                 for (int q = 0; q < winner; ++q) sw = tb_smax(2.0 * sw, alpha0);
                 shift = sw;
                 Lw = Lbase + winner * lpg;
-                if (t < nf) RD[t] = 1.0 / Lat(t, t);
+                if (t < nf) RD[t] = __drcp_rn(Lat(t, t));
                 sync();
                 return 0;
             }

@@ -560,7 +560,7 @@ struct Warp {
                 Lw = L + w * D * D;
                 if (lane < D) {
                     const double dii = Lw[lane + lane * D];
-                    RD[lane] = inF ? 1.0 / dii : 1.0;
+                    RD[lane] = inF ? __drcp_rn(dii) : 1.0;  // RN(1/d): the bits of 1.0 / d
                 }
                 __syncwarp();
                 return 0;
