@@ -141,7 +141,7 @@ int tb_context_create(const int32_t* devices, int32_t n_devices, tb_context** ou
         DevState d;
         d.device = devices ? devices[k] : k;
         if (d.device < 0 || d.device >= ndev) {
-            delete ctx;
+            tb_context_destroy(ctx);  // releases the devices set up so far
             return set_err(TB_E_INVALID_ARGUMENT, "tb_context_create: device %d out of range (%d visible)",
                            d.device, ndev);
         }
@@ -152,7 +152,8 @@ int tb_context_create(const int32_t* devices, int32_t n_devices, tb_context** ou
         if (e == cudaSuccess) e = cudaEventCreateWithFlags(&d.fork, cudaEventDisableTiming);
         if (e == cudaSuccess) e = cudaEventCreateWithFlags(&d.join, cudaEventDisableTiming);
         if (e != cudaSuccess) {
-            delete ctx;
+            ctx->devs.push_back(d);  // the partially created streams / events are released with it
+            tb_context_destroy(ctx);
             cudaSetDevice(prev);
             return set_err(TB_E_CUDA, "tb_context_create: %s", cudaGetErrorString(e));
         }
@@ -169,7 +170,7 @@ int tb_context_destroy(tb_context* ctx) {
     cudaGetDevice(&prev);
     for (auto& d : ctx->devs) {
         cudaSetDevice(d.device);
-        cudaStreamSynchronize(d.stream);
+        if (d.stream) cudaStreamSynchronize(d.stream);
         for (auto& a : d.aux)
             if (a) cudaStreamSynchronize(a);
         for (auto& e : d.ev)
@@ -440,6 +441,10 @@ extern "C" int tb_solve_batch(tb_context* ctx, const tb_problem_batch* b, const 
     const bool out_host = r->memspace == TB_MEM_HOST;
     int prev = 0;
     cudaGetDevice(&prev);
+    struct Restore {
+        int dev;
+        ~Restore() { cudaSetDevice(dev); }
+    } restore{prev};  // every return path leaves the caller's device current
     const auto t0 = clock::now();
 
     r->n_partitions = G;
@@ -595,6 +600,7 @@ extern "C" int tb_solve_batch(tb_context* ctx, const tb_problem_batch* b, const 
         CUDA_TRY(cudaMemcpyAsync(d.flag.p, &init, sizeof init, cudaMemcpyHostToDevice, d.stream));
         first_error_kernel<<<(unsigned)((c + 255) / 256), 256, 0, d.stream>>>(
             st_dev, c, static_cast<unsigned long long*>(d.flag.p));
+        CUDA_TRY(cudaGetLastError());
         tbdev::note_launches(1);
         unsigned long long idx = ~0ull;
         CUDA_TRY(cudaMemcpyAsync(&idx, d.flag.p, sizeof idx, cudaMemcpyDeviceToHost, d.stream));
@@ -606,7 +612,6 @@ extern "C" int tb_solve_batch(tb_context* ctx, const tb_problem_batch* b, const 
             bad_status = s;
         }
     }
-    cudaSetDevice(prev);
     if (first_bad >= 0)
         return set_err(TB_E_PROBLEM, "problem %lld: %s", (long long)first_bad, status_message(bad_status));
     return TB_OK;
