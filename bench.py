@@ -139,6 +139,13 @@ def cpu_sample(full_batch, seconds_target=1.5, workers=1, rate_guess=15000.0):
                         full_batch.params[:n], full_batch.x0[:n]), n
 
 
+def c2_config(n, world):
+    """The C2 workload description shared by both arms' JSON lines."""
+    return {"workload": WORKLOAD, "family": "branch", "dim": DIM, "batch_per_gpu": n, "global_batch": world * n,
+            "seed": "2+rank", "parallelism": f"batch sharded over {world} GPU(s)",
+            "l2": "flushed (256 MiB write) between timed steps, outside the events", "mode": "exact"}
+
+
 def run_reference_arm(args, rank, world):
     if rank != 0:
         return 0
@@ -164,7 +171,8 @@ def run_reference_arm(args, rank, world):
         "impl": "reference", "metric": METRIC, "value": value, "unit": "solves/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * wall / args.steps,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": WORKLOAD, "family": "branch", "dim": DIM, "batch": BATCH, "seed": 2},
+        "config": dict(c2_config(BATCH, world), l2="n/a (host CPU)",
+                       parallelism=f"reference solve_batch, std::thread over {cores} host cores"),
         "cpu_baseline": {"value": value, "unit": "solves/s", "cores": cores, "kind": "reference",
                          "sample": f"first {n} of the {BATCH} C2 problems per step, reference solve_batch(workers={cores})"},
         "e2e": {"value": value, "unit": "solves/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -499,9 +507,7 @@ def main():
             "metric": METRIC, "value": value, "unit": "solves/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": WORKLOAD, "family": "branch", "dim": DIM, "batch_per_gpu": N,
-                       "global_batch": world * N, "seed": "2+rank", "parallelism": f"batch sharded over {world} GPU(s)",
-                       "l2": "flushed (256 MiB write) between timed steps, outside the events", "mode": "exact"},
+            "config": c2_config(N, world),
             "e2e": {"value": e2e_value, "unit": "solves/s", "h2d_bytes_per_step": int(h2d),
                     "d2h_bytes_per_step": int(d2h)},
             "roofline": {"bound": "fp64", "achieved": achieved_tflops, "peak": fp64_peak, "unit": "TFLOP/s",
