@@ -37,6 +37,14 @@ while time.time() < t_end:
         b.upper[eq] = b.lower[eq]  # fixed variables (never free: strict inequalities)
     if rng.random() < 0.3:
         x0 = x0 * rng.uniform(1.5, 6.0)  # starts outside the box (projected)
+    if fam == "boxqp" and rng.random() < 0.25:  # extreme scales: quotients outside the Markstein range
+        hs, cs = 10.0 ** rng.uniform(-300, 250), 10.0 ** rng.uniform(-250, 250)
+        xs = 10.0 ** rng.uniform(-250, 250)
+        b.params[:, :d * d] *= hs
+        b.params[:, d * d:] *= cs
+        b.lower *= xs
+        b.upper *= xs
+        x0 = x0 * xs
     kw = {}
     r = rng.random()
     if r < 0.15:
@@ -47,7 +55,7 @@ while time.time() < t_end:
         kw = dict(cg_tol=float(rng.uniform(0.01, 0.9)), mu0=float(rng.uniform(0.001, 0.5)),
                   interp_factor=float(rng.uniform(0.1, 0.9)))
     elif r < 0.55:
-        kw = dict(tol_pg=float(10.0 ** rng.uniform(-10, -3)))
+        kw = dict(tol_pg=float(10.0 ** rng.uniform(-300, -3)))
     cfg = TronConfig(**kw)
     try:
         res = s.solve_batch(b, x0, cfg=cfg)
