@@ -8,7 +8,7 @@
 //                          branch's augmented-Lagrangian loop in one launch
 //   [exchange]             the caller all-gathers the branch solutions x
 //                          (NCCL over NVLink when sharded; nothing when not)
-//   admm_bus_kernel        bus consensus + multipliers + residual terms (every
+//   admm_bus_warp_kernel   bus consensus + multipliers + residual terms (every
 //                          bus, deterministic; residual max over this shard's
 //                          buses -> the caller max-allreduces two doubles)
 #include <cuda_runtime.h>
@@ -37,18 +37,145 @@ __device__ __forceinline__ void atomic_max_nonneg(unsigned long long* a, double 
     atomicMax(a, (unsigned long long)__double_as_longlong(x));
 }
 
-__global__ void admm_bus_kernel(tb_admm_view v, int res_lo, int res_hi, unsigned long long* res) {
-    const int b = blockIdx.x * blockDim.x + threadIdx.x;
-    tb_admm_res r = {0.0, 0.0};
+// The same bus pass (tb_admm_bus_update) with one warp per bus: lane k
+// evaluates item k of the bus's canonical list (its generators, then its
+// branch ends) -- the flows, quotients and per-coupling updates are
+// independent per item -- and the ordered sums are formed from the staged
+// terms in list order, so every sum, every multiplier and the residuals carry
+// the bits of the serial form (max is order-free: NaN never enters, as in
+// the serial `if (pr < d)`).  Serial per-bus work was the pass's latency
+// (one thread walked a hub bus's ends with dependent loads and divisions).
+constexpr int kBusWarps = 4;  // buses per block
+__global__ void __launch_bounds__(32 * kBusWarps)
+    admm_bus_warp_kernel(tb_admm_view v, int res_lo, int res_hi, unsigned long long* res) {
+    __shared__ double stage[kBusWarps][8][32];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int b = blockIdx.x * kBusWarps + w;
+    double (*T)[32] = stage[w];
+    double pr = 0.0, du = 0.0;
     if (b < v.n_bus) {
-        tb_admm_bus_update(&v, b, &r);
-        if (b < res_lo || b >= res_hi) r.primal = r.dual = 0.0;
-        if (!(r.primal >= 0.0)) r.primal = CUDART_INF;  // NaN -> report as inf
-        if (!(r.dual >= 0.0)) r.dual = CUDART_INF;
+        const int D = v.branch_dim;
+        const int g0 = v.gen_ptr[b], ng = v.gen_ptr[b + 1] - g0;
+        const int e0 = v.end_ptr[b], ne = v.end_ptr[b + 1] - e0;
+        const int cnt = ng + ne;
+        double SP = 0.0, WP = 0.0, SQ = 0.0, WQ = 0.0, Sw = 0.0, Rw = 0.0, St = 0.0, Rt = 0.0;
+        // pass 1: terms per item (lane), ordered sums over the list
+        for (int c0 = 0; c0 < cnt; c0 += 32) {
+            const int k = c0 + lane;
+            if (k < ng) {
+                const int g = v.gen_idx[g0 + k];
+                const double rp = v.gen_rp[g], rq = v.gen_rq[g];
+                T[0][lane] = v.gen_p[g] + v.gen_lp[g] / rp;
+                T[1][lane] = 1.0 / rp;
+                T[2][lane] = v.gen_q[g] + v.gen_lq[g] / rq;
+                T[3][lane] = 1.0 / rq;
+            } else if (k < cnt) {
+                const int e = v.end_idx[e0 + k - ng], l = e >> 1, end = e & 1;
+                const double* prm = v.br_params + (long)l * TB_BR_NPARAMS;
+                const double* x = v.br_x + (long)l * D;
+                double base[8];
+                tb_br_base(x, base);
+                const int fp = 2 * end, fq = 2 * end + 1;
+                T[0][lane] = tb_admm_flow(base, prm, fp) + prm[TB_BR_LAM + fp] / prm[TB_BR_RHO + fp];
+                T[1][lane] = 1.0 / prm[TB_BR_RHO + fp];
+                T[2][lane] = tb_admm_flow(base, prm, fq) + prm[TB_BR_LAM + fq] / prm[TB_BR_RHO + fq];
+                T[3][lane] = 1.0 / prm[TB_BR_RHO + fq];
+                const double vv = x[end];
+                const double rw = prm[TB_BR_RHOW + end], rt = prm[TB_BR_RHOT + end];
+                T[4][lane] = rw * (vv * vv + prm[TB_BR_LAMW + end] / rw);
+                T[5][lane] = rw;
+                T[6][lane] = rt * (x[2 + end] + prm[TB_BR_LAMT + end] / rt);
+                T[7][lane] = rt;
+            }
+            __syncwarp();
+            const int m = min(32, cnt - c0);
+            for (int q = 0; q < m; ++q) {
+                if (c0 + q < ng) {
+                    SP += T[0][q];
+                    WP += T[1][q];
+                    SQ += T[2][q];
+                    WQ += T[3][q];
+                } else {
+                    SP -= T[0][q];
+                    WP += T[1][q];
+                    SQ -= T[2][q];
+                    WQ += T[3][q];
+                    Sw += T[4][q];
+                    Rw += T[5][q];
+                    St += T[6][q];
+                    Rt += T[7][q];
+                }
+            }
+            __syncwarp();  // the next chunk rewrites the staging
+        }
+        // the bus's closed form (every lane, identical bits)
+        const double pd = v.bus_pd[b], qd = v.bus_qd[b];
+        const double aPw = -v.bus_gsh[b], aQw = v.bus_bsh[b];
+        const double mbar = Sw / Rw;
+        const double r1 = (SP + aPw * mbar) - pd;
+        const double r2 = (SQ + aQw * mbar) - qd;
+        const double A12 = (aPw * aQw) / Rw;
+        double muP, muQ;
+        if (A12 == 0.0) {
+            muP = r1 / (WP + (aPw * aPw) / Rw);
+            muQ = r2 / (WQ + (aQw * aQw) / Rw);
+        } else {
+            const double A11 = WP + (aPw * aPw) / Rw, A22 = WQ + (aQw * aQw) / Rw;
+            const double det = A11 * A22 - A12 * A12;
+            muP = (r1 * A22 - A12 * r2) / det;
+            muQ = (A11 * r2 - A12 * r1) / det;
+        }
+        const double wt = mbar - (aPw * muP + aQw * muQ) / Rw;
+        const double tt = St / Rt;
+        // pass 2: consensus, multipliers and residual terms per item
+        auto coupling = [&](double x, double xt_old, double xt_new, double rho, double& lam) {
+            const double d_ = tb_admm_absd(rho * (xt_new - xt_old));
+            if (du < d_) du = d_;
+            const double g_ = x - xt_new;
+            if (pr < tb_admm_absd(g_)) pr = tb_admm_absd(g_);
+            lam += rho * g_;
+        };
+        for (int k = lane; k < cnt; k += 32) {
+            if (k < ng) {
+                const int g = v.gen_idx[g0 + k];
+                const double rp = v.gen_rp[g], rq = v.gen_rq[g];
+                const double ptn = (v.gen_p[g] + v.gen_lp[g] / rp) - muP / rp;
+                const double qtn = (v.gen_q[g] + v.gen_lq[g] / rq) - muQ / rq;
+                coupling(v.gen_p[g], v.gen_pt[g], ptn, rp, v.gen_lp[g]);
+                coupling(v.gen_q[g], v.gen_qt[g], qtn, rq, v.gen_lq[g]);
+                v.gen_pt[g] = ptn;
+                v.gen_qt[g] = qtn;
+            } else {
+                const int e = v.end_idx[e0 + k - ng], l = e >> 1, end = e & 1;
+                double* prm = v.br_params + (long)l * TB_BR_NPARAMS;
+                const double* x = v.br_x + (long)l * D;
+                double base[8];
+                tb_br_base(x, base);
+                const int fp = 2 * end, fq = 2 * end + 1;
+                const double Fp = tb_admm_flow(base, prm, fp), Fq = tb_admm_flow(base, prm, fq);
+                const double rP = prm[TB_BR_RHO + fp], rQ = prm[TB_BR_RHO + fq];
+                const double Ftp = (Fp + prm[TB_BR_LAM + fp] / rP) + muP / rP;
+                const double Ftq = (Fq + prm[TB_BR_LAM + fq] / rQ) + muQ / rQ;
+                coupling(Fp, prm[TB_BR_TIL + fp], Ftp, rP, prm[TB_BR_LAM + fp]);
+                coupling(Fq, prm[TB_BR_TIL + fq], Ftq, rQ, prm[TB_BR_LAM + fq]);
+                prm[TB_BR_TIL + fp] = Ftp;
+                prm[TB_BR_TIL + fq] = Ftq;
+                const double vv = x[end];
+                coupling(vv * vv, prm[TB_BR_WTIL + end], wt, prm[TB_BR_RHOW + end], prm[TB_BR_LAMW + end]);
+                coupling(x[2 + end], prm[TB_BR_TTIL + end], tt, prm[TB_BR_RHOT + end], prm[TB_BR_LAMT + end]);
+                prm[TB_BR_WTIL + end] = wt;
+                prm[TB_BR_TTIL + end] = tt;
+            }
+        }
+        if (lane == 0) {
+            v.bus_wt[b] = wt;
+            v.bus_tt[b] = tt;
+        }
+        if (b < res_lo || b >= res_hi) pr = du = 0.0;
     }
-    const double p = tbdev::warp_max_nonneg(r.primal);
-    const double d = tbdev::warp_max_nonneg(r.dual);
-    if ((threadIdx.x & 31) == 0) {
+    const double p = tbdev::warp_max_nonneg(pr);
+    const double d = tbdev::warp_max_nonneg(du);
+    if (lane == 0) {
         atomic_max_nonneg(res + 0, p);
         atomic_max_nonneg(res + 1, d);
     }
@@ -409,8 +536,8 @@ int tb_admm_update_consensus(tb_admm* a, void* stream, double* res2_dev) {
     cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : a->stream;
     a->last = st;
     cudaMemsetAsync(a->res, 0, 2 * sizeof(unsigned long long), st);
-    // 32-thread blocks: one bus per thread with serial per-bus work, spread over every SM
-    admm_bus_kernel<<<(a->v.n_bus + 31) / 32, 32, 0, st>>>(a->v, a->bus_lo, a->bus_hi, a->res);
+    admm_bus_warp_kernel<<<(a->v.n_bus + kBusWarps - 1) / kBusWarps, 32 * kBusWarps, 0, st>>>(a->v, a->bus_lo,
+                                                                                             a->bus_hi, a->res);
     tbdev::note_launches(1);
     if (res2_dev) cudaMemcpyAsync(res2_dev, a->res, 2 * sizeof(double), cudaMemcpyDeviceToDevice, st);
     ++a->iterations;
