@@ -15,6 +15,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -24,6 +25,7 @@
 #include "tb_admm_host.h"
 #include "tron_device.cuh"
 #include "tron_launch.h"
+#include "tron_thread.cuh"
 
 namespace {
 
@@ -470,6 +472,15 @@ int tb_admm_destroy(tb_admm* a) {
 
 // generator update (all generators) + branch TRON on this shard, enqueued on
 // `stream` (NULL: the ADMM's own stream); returns without synchronising.
+// d = 4 branch stage form: thread per branch unless TB_ADMM_WARP=1
+static bool thread_form() {
+    static const bool t = [] {
+        const char* e = getenv("TB_ADMM_WARP");
+        return !(e && e[0] == '1');
+    }();
+    return t;
+}
+
 int tb_admm_solve_components(tb_admm* a, void* stream) {
     if (!a) return fail(TB_E_INVALID_ARGUMENT, "null admm");
     DeviceGuard guard(a->device);
@@ -496,12 +507,33 @@ int tb_admm_solve_components(tb_admm* a, void* stream) {
         k.extrap = 1.0 / a->tron.interp_factor;
         k.x_star = a->x + a->br_lo * 6;  // in place
         k.status = a->status + a->br_lo;
+        // (a thread-per-branch form of this loop measured 184 vs 283 iter/s on C4: the AL
+        // rounds make the stage throughput-bound, where the warp form wins)
         const size_t smem = sizeof(double) * (size_t)(tbdev::SmemLayout<6>::fixed() + TB_BR_NPARAMS);
         admm_auglag_fused_kernel<<<(unsigned)cnt, 32, smem, st>>>(
             k, a->v.br_params + a->br_lo * TB_BR_NPARAMS, a->eta + a->br_lo, a->opt.auglag_xi0, a->opt.auglag_eta0,
             a->opt.auglag_feas_tol, a->opt.auglag_xi_max, a->opt.auglag_max_iter, a->round_max);
         admm_round_accum_kernel<<<1, 1, 0, st>>>(a->round_max, a->rounds_total);
         tbdev::note_launches(2);
+    } else if (cnt > 0 && thread_form()) {
+        // one thread per branch (tron_thread.cuh): the stage waits for its
+        // slowest branch, whose latency this form cuts
+        tbdev::KernelArgs k{};
+        k.n = 4;
+        k.nparams = TB_BR_NPARAMS;
+        k.count = cnt;
+        k.stride = TB_BR_NPARAMS;
+        k.x0 = a->x + a->br_lo * 4;
+        k.lo = a->lower + a->br_lo * 4;
+        k.up = a->upper + a->br_lo * 4;
+        k.prm = a->v.br_params + a->br_lo * TB_BR_NPARAMS;
+        k.cfg = a->tron;
+        k.fast_forward = 1;
+        k.extrap = 1.0 / a->tron.interp_factor;
+        k.x_star = a->x + a->br_lo * 4;  // in place: each thread reads its x0 first
+        k.status = a->status + a->br_lo;
+        tbdev::tron_thread_kernel<4><<<(unsigned)((cnt + 63) / 64), 64, 0, st>>>(k);
+        tbdev::note_launches(1);
     } else if (cnt > 0) {
         tb_problem_batch b{TB_FAMILY_BRANCH, 4, cnt, a->x + a->br_lo * 4, a->lower + a->br_lo * 4,
                            a->upper + a->br_lo * 4, a->v.br_params + a->br_lo * TB_BR_NPARAMS, TB_BR_NPARAMS,
