@@ -39,6 +39,16 @@ METRIC = "bound-constrained solves/sec (batch, FP64)"
 WORKLOAD = "C2: 65,536 synthetic AC-OPF branch augmented-Lagrangian subproblems (d=6) per GPU"
 
 
+
+def kernel_form(d, count):
+    """Which device kernel the library routes a (dim, count) ncvx batch to
+    (csrc/tron_kernels_ncvx.cu, tron_thread.cuh)."""
+    if d == 4 and count >= int(os.environ.get("TB_THREAD_MIN", 8192)) and os.environ.get("TB_THREAD") != "0":
+        return "thread per problem"
+    if d <= 16:
+        return "warp per problem"
+    return f"block of {32 if d <= 32 else 64 if d <= 64 else 128} threads (persistent)"
+
 def env_int(k, d):
     try:
         return int(os.environ.get(k, d))
@@ -305,7 +315,7 @@ def run_sweep(args, dev, fp64_peak=None):
         flops = float(out_d.flops.sum().item())
         row = {"config": name, "family": "ncvx", "dim": d, "batch": B, "ms": ms, "solves_per_s": B / (ms * 1e-3),
                "achieved_tflops": flops / (ms * 1e-3) / 1e12, "flops_per_solve": flops / B,
-               "kernel": "warp per problem" if d <= 32 else f"block of {64 if d <= 64 else 128} threads (persistent)",
+               "kernel": kernel_form(d, B),
                "mean_iterations": float(out_d.iterations.double().mean().item()),
                "status_counts": {str(k): int(v) for k, v in
                                  zip(*np.unique(out_d.status.cpu().numpy(), return_counts=True))}}

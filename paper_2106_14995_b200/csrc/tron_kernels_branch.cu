@@ -1,8 +1,10 @@
 // tron_kernels_branch.cu — ADMM branch family kernels, D = dim exactly (4, 6).
 #include "tron_kernels.cuh"
+#include "tron_thread.cuh"
 
 namespace tbdev {
 cudaError_t launch_branch(const KernelArgs& a, cudaStream_t st) {
+    if (thread_form(a)) return launch_thread<4, TB_FAMILY_BRANCH>(a, st);
     if (a.n == 4) return launch_fd<TB_FAMILY_BRANCH, 4>(a, st);
     return launch_fd<TB_FAMILY_BRANCH, 6>(a, st);
 }

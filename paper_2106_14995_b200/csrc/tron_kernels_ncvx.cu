@@ -1,9 +1,11 @@
 // tron_kernels_ncvx.cu — TB_FAMILY_NCVX kernels: D = next of {4, 8, 16, 32} >= dim (one warp per
 // problem) up to d = 16; above it the block kernel with D = 32, 64 or 128 threads (tron_kernels.cuh).
 #include "tron_kernels.cuh"
+#include "tron_thread.cuh"
 
 namespace tbdev {
 cudaError_t launch_ncvx(const KernelArgs& a, cudaStream_t st) {
+    if (thread_form(a)) return launch_thread<4, TB_FAMILY_NCVX>(a, st);
     if (a.n <= 4) return launch_fd<TB_FAMILY_NCVX, 4>(a, st);
     if (a.n <= 8) return launch_fd<TB_FAMILY_NCVX, 8>(a, st);
     if (a.n >= blk_min_dim()) {

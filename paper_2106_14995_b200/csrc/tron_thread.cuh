@@ -1,4 +1,4 @@
-// tron_thread.cuh — one THREAD per problem (branch family, n = D = 4 or 6).
+// tron_thread.cuh — one THREAD per problem (branch and ncvx families, n = D <= 8).
 //
 // The warp kernel (tron_device.cuh) spreads one problem over a warp, which
 // maximises throughput on large batches, but every reduction / solve step of a
@@ -15,19 +15,78 @@
 // No flop counting (the COUNT variant stays in the warp kernel).
 #pragma once
 
+#include <cstdlib>
+
 #include "tron_device.cuh"
+#include "tron_launch.h"
 
 namespace tbdev {
 
+// per-thread family evaluation (the DevFamily expressions of tron_device.cuh
+// on one thread: same tb_families.h terms, same ascending sums)
+template <int FAM, int D>
+struct ThFam;
+
 template <int D>
+struct ThFam<TB_FAMILY_BRANCH, D> {
+    tb_branch_ctx ctx;
+    __device__ __forceinline__ void prepare(const double* x, const double* prm) { tb_branch_ctx_init(x, prm, D, &ctx); }
+    __device__ __forceinline__ double f(const double* prm) const { return tb_br_f(&ctx, prm, D); }
+    __device__ __forceinline__ double grad(const double*, int i) const { return tb_br_grad(&ctx, D, i); }
+    __device__ __forceinline__ double hess(const double* prm, int i, int j) const { return tb_br_hess(&ctx, prm, D, i, j); }
+};
+
+template <int D>
+struct ThFam<TB_FAMILY_NCVX, D> {
+    double e[D], he[D], sn[D], cs[D];  // x - c, H (x - c), sin x, cos x
+    static constexpr int NH = D * (D + 1) / 2;
+    __device__ __forceinline__ void prepare(const double* x, const double* prm) {
+        const double* c = prm + NH;
+#pragma unroll
+        for (int i = 0; i < D; ++i) {
+            e[i] = x[i] - c[i];
+            tb_sincos(x[i], &sn[i], &cs[i]);
+        }
+#pragma unroll
+        for (int i = 0; i < D; ++i) he[i] = tb_ncvx_he_i(x, prm, D, i);
+    }
+    __device__ __forceinline__ double f(const double* prm) const {
+        const double* k = prm + NH + D;
+        const double* a = k + D;
+        double q = 0.0, quart = 0.0, s = 0.0;
+#pragma unroll
+        for (int i = 0; i < D; ++i) {
+            const double e2 = e[i] * e[i];
+            q += e[i] * he[i];
+            quart += k[i] * (e2 * e2);
+            s += a[i] * sn[i];
+        }
+        return (0.5 * q + 0.25 * quart) + s;
+    }
+    __device__ __forceinline__ double grad(const double* prm, int i) const {
+        const double* k = prm + NH + D;
+        const double* a = k + D;
+        const double e3 = (e[i] * e[i]) * e[i];
+        return (he[i] + k[i] * e3) + a[i] * cs[i];
+    }
+    __device__ __forceinline__ double hess(const double* prm, int i, int j) const {
+        const double h = tb_ncvx_H(prm, D, i, j);
+        if (i != j) return h;
+        const double* k = prm + NH + D;
+        const double* a = k + D;
+        return (h + (3.0 * k[i]) * (e[i] * e[i])) - a[i] * sn[i];
+    }
+};
+
+template <int D, int FAM = TB_FAMILY_BRANCH>
 struct Th {
-    static_assert(D == 4 || D == 6, "thread form: branch family only");
+    static_assert(D <= 8, "thread form: small problems only");
     double A[D * D];  // column-major Hessian
     double L[D * D];  // factor (lower), column-major
     const double* prm;
     const tb_tron_config* cfg;
     double extrap;
-    tb_branch_ctx ctx;
+    ThFam<FAM, D> fam;
 
     // ------------------------------------------------ dense.hpp BLAS (ordered)
     __device__ __forceinline__ static bool in(unsigned m, int i) { return (m >> i) & 1u; }
@@ -427,10 +486,10 @@ struct Th {
 // tron.hpp:453-549 solve() of problem `pid` by the calling thread (the warp
 // kernel's loop structure: one evaluation site, fast-forward of the
 // zero-change fixed point).
-template <int D>
+template <int D, int FAM = TB_FAMILY_BRANCH>
 __device__ __forceinline__ void tron_solve_thread(const KernelArgs& a, const long long pid) {
     const unsigned long long t_start = globaltimer();
-    Th<D> W;
+    Th<D, FAM> W;
     W.prm = a.prm + pid * a.stride;
     W.cfg = &a.cfg;
     W.extrap = a.extrap;
@@ -458,7 +517,7 @@ __device__ __forceinline__ void tron_solve_thread(const KernelArgs& a, const lon
         const double kEta1 = 0.25, kEta2 = 0.75;
 #pragma unroll
         for (int i = 0; i < D; ++i) {
-            x[i] = Th<D>::clip(x[i], l[i], u[i]);
+            x[i] = Th<D, FAM>::clip(x[i], l[i], u[i]);
             xe[i] = x[i];
         }
         double delta = 0.0, alpha_c = 1.0, delta_in = 0.0, alpha_in = 0.0;
@@ -466,8 +525,8 @@ __device__ __forceinline__ void tron_solve_thread(const KernelArgs& a, const lon
         long long cg_its = 0;
 #pragma unroll 1
         for (int iter = 0;; ++iter) {
-            tb_branch_ctx_init(xe, W.prm, n, &W.ctx);
-            const double fe = tb_br_f(&W.ctx, W.prm, n);
+            W.fam.prepare(xe, W.prm);
+            const double fe = W.fam.f(W.prm);
             ++f_evals;
             bool take = iter == 0;
             if (iter > 0) {
@@ -509,11 +568,11 @@ __device__ __forceinline__ void tron_solve_thread(const KernelArgs& a, const lon
             }
             if (take) {
 #pragma unroll
-                for (int i = 0; i < D; ++i) g[i] = tb_br_grad(&W.ctx, n, i);
-                pg = Th<D>::pgnorm(x, g, l, u, n);
+                for (int i = 0; i < D; ++i) g[i] = W.fam.grad(W.prm, i);
+                pg = Th<D, FAM>::pgnorm(x, g, l, u, n);
             }
             if (iter == 0) {
-                delta = cfg.has_delta0 ? cfg.delta0 : tb_smax(Th<D>::nrm2(g, act), 1.0);
+                delta = cfg.has_delta0 ? cfg.delta0 : tb_smax(Th<D, FAM>::nrm2(g, act), 1.0);
                 status = pg <= cfg.tol_pg ? TB_STATUS_CONVERGED : TB_STATUS_ITER_LIMIT;
                 if (status == TB_STATUS_CONVERGED) break;
             } else {
@@ -537,7 +596,7 @@ __device__ __forceinline__ void tron_solve_thread(const KernelArgs& a, const lon
                 for (int j = 0; j < D; ++j)
 #pragma unroll
                     for (int i = j; i < D; ++i) {
-                        const double h = tb_br_hess(&W.ctx, W.prm, n, i, j);
+                        const double h = W.fam.hess(W.prm, i, j);
                         W.A[i + j * D] = h;
                         W.A[j + i * D] = h;
                     }
@@ -572,11 +631,32 @@ __device__ __forceinline__ void tron_solve_thread(const KernelArgs& a, const lon
     if (a.wall_time) a.wall_time[pid] = 1e-9 * (double)(globaltimer() - t_start);
 }
 
-template <int D>
+// Routing (host): the thread form takes n = 4 batches of at least
+// TB_THREAD_MIN problems (default 8192; C3 ncvx d=4 x32768: 0.97 vs 1.40 ms,
+// branch d=4 x65536: 1.12 vs 3.09 ms; at 1,024 problems the warp form's
+// shorter per-problem latency wins, 0.30 vs 0.70 ms; at n = 6 / 8 the 255-
+// register thread form loses, 7.7 vs 7.4 ms branch6, 13.3 vs 3.6 ms ncvx8).
+// TB_THREAD=0 forces the warp form.  Flop counting stays in the warp kernel.
+inline bool thread_form(const KernelArgs& a) {
+    if (a.flops || a.n != 4) return false;
+    const char* e = getenv("TB_THREAD");
+    if (e && e[0] == '0') return false;
+    const char* m = getenv("TB_THREAD_MIN");
+    return a.count >= (m ? atoll(m) : 8192LL);
+}
+
+template <int D, int FAM = TB_FAMILY_BRANCH>
 __global__ void __launch_bounds__(64) tron_thread_kernel(const __grid_constant__ KernelArgs a) {
     const long long pid = blockIdx.x * (long long)blockDim.x + threadIdx.x;
     if (pid >= a.count) return;
-    tron_solve_thread<D>(a, pid);
+    tron_solve_thread<D, FAM>(a, pid);
+}
+
+template <int D, int FAM>
+inline cudaError_t launch_thread(const KernelArgs& a, cudaStream_t st) {
+    tron_thread_kernel<D, FAM><<<(unsigned)((a.count + 63) / 64), 64, 0, st>>>(a);
+    note_launches(1);
+    return cudaGetLastError();
 }
 
 }  // namespace tbdev

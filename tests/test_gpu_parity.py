@@ -367,3 +367,62 @@ def test_extreme_scales_take_the_ieee_division_path(solver, d, h_scale, c_scale,
     ref = po.solve_batch(sb, cfg=cfg, impl="oracle", workers=8)
     assert_bitwise(res, ref, label=f"d={d} h={h_scale} c={c_scale}")
     assert np.array_equal(host(res.flops), ref.flops)
+
+
+# ---------------------------------------------------------------- thread form
+# n = 4 batches of >= TB_THREAD_MIN problems (default 8192) run one thread per
+# problem (csrc/tron_thread.cuh); these pin it to the oracle and to the warp
+# form (TB_THREAD=0), also on small batches forced through it (TB_THREAD_MIN=1).
+
+
+@pytest.mark.parametrize("fam", ["ncvx", "branch"])
+def test_thread_form_default_routing_bitwise(solver, monkeypatch, fam):
+    b = synth.make(fam, 16384, 4)
+    res = solver.solve_batch(b)  # >= 8192 problems: thread form
+    ref = po.solve_batch(b, impl="oracle", workers=os.cpu_count() or 8)
+    assert_bitwise(res, ref, label=f"{fam}4 thread form")
+    monkeypatch.setenv("TB_THREAD", "0")
+    assert_bitwise(solver.solve_batch(b), ref, label=f"{fam}4 warp form")
+
+
+@pytest.mark.parametrize("cfg", [TronConfig(), TronConfig(max_iter=1), TronConfig(delta0=0.3), TronConfig(tol_pg=1e-9),
+                                 TronConfig(cg_tol=0.5, mu0=0.1, interp_factor=0.25),
+                                 TronConfig(sigma1=0.1, sigma2=0.3, sigma3=2.0, eta0=0.01, delta_max=5.0)])
+def test_thread_form_config_variants_bitwise(solver, monkeypatch, cfg):
+    monkeypatch.setenv("TB_THREAD_MIN", "1")
+    for b in (synth.ncvx(300, 4, seed=9), synth.branch(300, 4, seed=9)):
+        assert_bitwise(solver.solve_batch(b, cfg=cfg), po.solve_batch(b, cfg=cfg, impl="oracle"),
+                       label=f"thread form {cfg}")
+
+
+def test_thread_form_outside_box_infinite_bounds_and_bad_bounds(solver, monkeypatch):
+    monkeypatch.setenv("TB_THREAD_MIN", "1")
+    b = synth.ncvx(200, 4, seed=11)
+    b.lower[::3, 1] = -np.inf
+    b.upper[::4, 2] = np.inf
+    x0 = b.x0 * 5.0
+    res = solver.solve_batch(b, x0)
+    assert_bitwise(res, po.solve_batch(b, x0, impl="oracle"), label="thread form outside/inf")
+    xs = host(res.x_star)
+    assert (xs >= b.lower).all() and (xs <= b.upper).all()
+    b.lower[7, 0] = b.upper[7, 0] + 1.0
+    with pytest.raises(ValueError, match="lower bound exceeds upper bound"):
+        solver.solve_batch(b)
+
+
+def test_thread_form_ragged_counts_and_device_memspace(solver, monkeypatch):
+    import torch
+
+    from paper_2106_14995_b200 import ProblemBatch, Solver
+
+    monkeypatch.setenv("TB_THREAD_MIN", "1")
+    for n in (1, 63, 64, 65, 129):
+        b = synth.ncvx(n, 4, seed=20 + n)
+        assert_bitwise(solver.solve_batch(b), po.solve_batch(b, impl="oracle"), label=f"thread form n={n}")
+    b = synth.branch(1000, 4, seed=3)
+    dev = torch.device("cuda", 0)
+    t = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(dev)  # noqa: E731
+    db = ProblemBatch(b.family, 4, t(b.lower), t(b.upper), t(b.params), t(b.x0))
+    out = Solver.alloc_result(1000, 4, device=True)
+    solver.solve_batch(db, out=out)
+    assert_bitwise(out, po.solve_batch(b, impl="oracle"), label="thread form device memspace")
