@@ -83,6 +83,7 @@ struct Th {
     static_assert(D <= 8, "thread form: small problems only");
     double A[D * D];  // column-major Hessian
     double L[D * D];  // factor (lower), column-major
+    double rd[D];     // RN(1 / L(j,j)) of the current factor
     const double* prm;
     const tb_tron_config* cfg;
     double extrap;
@@ -191,6 +192,9 @@ struct Th {
     }
 
     // ------------------------------------------------ dense.hpp:182-201 ccf
+    // column j's quotients col[i] / d as Markstein quotients from one
+    // RN(1/d) (tron_device.cuh quot: correctly rounded, bits of the division);
+    // a column that met an out-of-range quotient is redone with IEEE divisions
     __device__ __forceinline__ bool chol(unsigned F, double sh) {
 #pragma unroll
         for (int j = 0; j < D; ++j) {
@@ -212,10 +216,18 @@ struct Th {
             const double pivot = col[j];
             if (!(pivot > 0.0)) return false;
             const double d = sqrt(pivot);
+            const double r = __drcp_rn(d);
             L[j + j * D] = d;
+            rd[j] = r;
+            bool bad = false;
 #pragma unroll
             for (int i = j + 1; i < D; ++i)
-                if (in(F, i)) L[i + j * D] = col[i] / d;
+                if (in(F, i)) L[i + j * D] = quot<false>(col[i], d, r, bad);
+            if (bad) {
+#pragma unroll
+                for (int i = j + 1; i < D; ++i)
+                    if (in(F, i)) L[i + j * D] = col[i] / d;
+            }
         }
         return true;
     }
@@ -246,7 +258,11 @@ struct Th {
         return TB_STATUS_FACTORIZATION_FAILED;
     }
     // dense.hpp:224-228 / 229-235 on F (entries outside F: forward 0, backward pass-through)
-    __device__ __forceinline__ void trsv_fwd(const double* b, unsigned F, double* y) const {
+    // quotients by L(i,i) from the stored RN(1/L(i,i)); one range test per
+    // solve, a solve that met an out-of-range quotient reruns with IEEE
+    template <bool IEEE>
+    __device__ __forceinline__ bool trsv_fwd_q(const double* b, unsigned F, double* y) const {
+        bool bad = false;
 #pragma unroll
         for (int i = 0; i < D; ++i) {
             if (!in(F, i)) {
@@ -257,10 +273,13 @@ struct Th {
 #pragma unroll
             for (int j = 0; j < i; ++j)
                 if (in(F, j)) s -= L[i + j * D] * y[j];
-            y[i] = s / L[i + i * D];
+            y[i] = quot<IEEE>(s, L[i + i * D], rd[i], bad);
         }
+        return bad;
     }
-    __device__ __forceinline__ void trsv_bwd(const double* b, unsigned F, double* y) const {
+    template <bool IEEE>
+    __device__ __forceinline__ bool trsv_bwd_q(const double* b, unsigned F, double* y) const {
+        bool bad = false;
 #pragma unroll
         for (int i = D - 1; i >= 0; --i) {
             if (!in(F, i)) {
@@ -271,8 +290,16 @@ struct Th {
 #pragma unroll
             for (int j = i + 1; j < D; ++j)
                 if (in(F, j)) s -= L[j + i * D] * y[j];
-            y[i] = s / L[i + i * D];
+            y[i] = quot<IEEE>(s, L[i + i * D], rd[i], bad);
         }
+        return bad;
+    }
+    // dense.hpp:224-228 / 229-235 on F (entries outside F: forward 0, backward pass-through)
+    __device__ __forceinline__ void trsv_fwd(const double* b, unsigned F, double* y) const {
+        if (trsv_fwd_q<false>(b, F, y)) trsv_fwd_q<true>(b, F, y);
+    }
+    __device__ __forceinline__ void trsv_bwd(const double* b, unsigned F, double* y) const {
+        if (trsv_bwd_q<false>(b, F, y)) trsv_bwd_q<true>(b, F, y);
     }
 
     // ------------------------------------------------ tron.hpp:290-344 PCG

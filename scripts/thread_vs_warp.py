@@ -1,4 +1,4 @@
-"""Branch family: warp-per-problem vs thread-per-problem (TB_BRANCH_THREAD=1), device-resident
+"""Branch family: warp-per-problem vs thread-per-problem (TB_THREAD=0 forces the warp form), device-resident
 timing and bitwise comparison of every SolveReport field.
 python scripts/thread_vs_warp.py [n [fam,fam [variant,variant]]]"""
 import os, subprocess, sys
@@ -21,16 +21,16 @@ ts = []
 for _ in range(7):
     s.solve_batch(db, out=out); ts.append(out.kernel_time)
 ts.sort()
-np.savez('/tmp/tvw_%s_%s.npz' % (fam, os.environ.get('TB_BRANCH_THREAD', '0')),
+np.savez('/tmp/tvw_%s_%s.npz' % (fam, os.environ.get('TB_THREAD', '0')),
          **{k: getattr(out, k).cpu().numpy() for k in ('x_star', 'f_star', 'pg_norm', 'status', 'iterations', 'cg_iterations', 'f_evals')})
-print(f"thread={os.environ.get('TB_BRANCH_THREAD','0')} {fam} x{n}: best {ts[0]*1e3:.3f} ms  median {ts[3]*1e3:.3f} ms")
+print(f"TB_THREAD={os.environ.get("TB_THREAD")} {fam} x{n}: best {ts[0]*1e3:.3f} ms  median {ts[3]*1e3:.3f} ms")
 """
 import numpy as np
 fams = sys.argv[2].split(",") if len(sys.argv) > 2 else ["branch6", "branch4"]
 variants = sys.argv[3].split(",") if len(sys.argv) > 3 else ["0", "1"]
 for fam in fams:
     for thr in variants:
-        env = dict(os.environ, VT_FAM=fam, VT_N=str(n), TB_BRANCH_THREAD=thr)
+        env = dict(os.environ, VT_FAM=fam, VT_N=str(n), TB_THREAD=thr)
         p = subprocess.run([sys.executable, "-c", CODE], env=env, capture_output=True, text=True)
         print(p.stdout.strip() or p.stderr[-1500:], flush=True)
     try:

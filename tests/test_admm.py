@@ -236,18 +236,28 @@ def test_device_admm_c4_first_iterations_bitwise():
     assert np.array_equal(dev.get(A.BRANCH_PARAMS), cpu.get(A.BRANCH_PARAMS))
 
 
-@pytest.mark.gpu
-def test_sharded_path_world1_equals_single():
-    """The torch.distributed driver (C5 path) at world size 1 == AdmmSolver."""
+@pytest.fixture(scope="module")
+def nccl_world1():
+    """A world-size-1 NCCL group for the sharded-driver tests, torn down after them."""
+    import os
+
     import torch.distributed as dist
 
-    g = synth.grid(500, 700, 150, seed=2)
+    created = False
     if not dist.is_initialized():
-        import os
-
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
         os.environ.setdefault("MASTER_PORT", "29533")
         dist.init_process_group("nccl", rank=0, world_size=1)
+        created = True
+    yield
+    if created:
+        dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+def test_sharded_path_world1_equals_single(nccl_world1):
+    """The torch.distributed driver (C5 path) at world size 1 == AdmmSolver."""
+    g = synth.grid(500, 700, 150, seed=2)
     sh = A.ShardedAdmm(g, 0, 1, 0)
     ref = A.AdmmSolver(g)
     for k in range(10):
@@ -273,17 +283,9 @@ def test_device_admm_line_limits_bitwise_vs_oracle():
 
 
 @pytest.mark.gpu
-def test_sharded_path_world1_line_limits_equals_single():
+def test_sharded_path_world1_line_limits_equals_single(nccl_world1):
     """The torch.distributed driver with the d=6 branch stage (x rows of 6)."""
-    import torch.distributed as dist
-
     g, _ = _binding_grid()
-    if not dist.is_initialized():
-        import os
-
-        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-        os.environ.setdefault("MASTER_PORT", "29534")
-        dist.init_process_group("nccl", rank=0, world_size=1)
     opts = A.AdmmOptions(line_limits=True)
     sh = A.ShardedAdmm(g, 0, 1, 0, opts)
     ref = A.AdmmSolver(g, opts)
