@@ -43,7 +43,7 @@ WORKLOAD = "C2: 65,536 synthetic AC-OPF branch augmented-Lagrangian subproblems 
 def kernel_form(d, count):
     """Which device kernel the library routes a (dim, count) ncvx batch to
     (csrc/tron_kernels_ncvx.cu, tron_thread.cuh)."""
-    if d == 4 and count >= int(os.environ.get("TB_THREAD_MIN", 8192)) and os.environ.get("TB_THREAD") != "0":
+    if d == 4 and count >= int(os.environ.get("TB_THREAD_MIN", 16384)) and os.environ.get("TB_THREAD") != "0":
         return "thread per problem"
     if d <= 16:
         return "warp per problem"

@@ -337,6 +337,7 @@ tbdev::KernelArgs make_args(const tb_problem_batch* b, int64_t np, const tb_tron
     a.flops = o.flops;
     a.ws = nullptr;
     a.ws_bytes = 0;
+    a.route_count = cnt;
     return a;
 }
 
@@ -529,6 +530,7 @@ extern "C" int tb_solve_batch(tb_context* ctx, const tb_problem_batch* b, const 
                       off(ofull.iters, 1), off(ofull.cg, 1),    off(ofull.fev, 1), off(ofull.flops, 1),
                       off(ofull.wall, 1)};
             tbdev::KernelArgs a = make_args(b, np, cfg, ctx->fast_forward, x0, lw, up, prm, stride, cc, o);
+            a.route_count = c;  // kernel-form routing by the partition, not the pipeline chunk
             CUDA_TRY(attach_ws(d, b->family, a));
             if (ch == 0) CUDA_TRY(cudaEventRecord(d.ev[1], st));
             if (!staged) CUDA_TRY(launch_split(d, b->family, a, st, device_chunks(b->family, n, cc)));

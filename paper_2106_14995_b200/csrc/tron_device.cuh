@@ -117,6 +117,9 @@ struct KernelArgs {
     // Hessian slices) and its size in bytes
     void* ws;
     size_t ws_bytes;
+    // problems of the whole batch / partition this launch is a chunk of
+    // (kernel-form routing, tron_thread.cuh thread_form); 0 = count
+    long long route_count;
 };
 
 // shared memory per warp (doubles; every region starts at an even offset)

@@ -4,7 +4,7 @@
 
 namespace tbdev {
 cudaError_t launch_branch(const KernelArgs& a, cudaStream_t st) {
-    if (thread_form(a)) return launch_thread<4, TB_FAMILY_BRANCH>(a, st);
+    if (thread_form(a, 4096)) return launch_thread<4, TB_FAMILY_BRANCH>(a, st);
     if (a.n == 4) return launch_fd<TB_FAMILY_BRANCH, 4>(a, st);
     return launch_fd<TB_FAMILY_BRANCH, 6>(a, st);
 }

@@ -5,7 +5,7 @@
 
 namespace tbdev {
 cudaError_t launch_ncvx(const KernelArgs& a, cudaStream_t st) {
-    if (thread_form(a)) return launch_thread<4, TB_FAMILY_NCVX>(a, st);
+    if (thread_form(a, 16384)) return launch_thread<4, TB_FAMILY_NCVX>(a, st);
     if (a.n <= 4) return launch_fd<TB_FAMILY_NCVX, 4>(a, st);
     if (a.n <= 8) return launch_fd<TB_FAMILY_NCVX, 8>(a, st);
     if (a.n >= blk_min_dim()) {

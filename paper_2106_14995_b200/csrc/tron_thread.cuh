@@ -658,18 +658,22 @@ __device__ __forceinline__ void tron_solve_thread(const KernelArgs& a, const lon
     if (a.wall_time) a.wall_time[pid] = 1e-9 * (double)(globaltimer() - t_start);
 }
 
-// Routing (host): the thread form takes n = 4 batches of at least
-// TB_THREAD_MIN problems (default 8192; C3 ncvx d=4 x32768: 0.97 vs 1.40 ms,
-// branch d=4 x65536: 1.12 vs 3.09 ms; at 1,024 problems the warp form's
-// shorter per-problem latency wins, 0.30 vs 0.70 ms; at n = 6 / 8 the 255-
-// register thread form loses, 7.7 vs 7.4 ms branch6, 13.3 vs 3.6 ms ncvx8).
-// TB_THREAD=0 forces the warp form.  Flop counting stays in the warp kernel.
-inline bool thread_form(const KernelArgs& a) {
+// Routing (host): the thread form takes n = 4 batches (the whole batch or
+// partition, not the concurrent chunk) of at least min_count problems: branch
+// 4,096, ncvx 16,384 (TB_THREAD_MIN overrides both).  Measured, device-
+// resident, thread vs warp: ncvx d=4 x32,768 0.95 vs 1.40 ms, x20,467 0.83
+// vs 0.97, x16,384 0.79 vs 0.81, x12,000 0.79 vs 0.66, x1,024 0.70 vs 0.30 (a
+// lone problem's chain is slower on one thread); branch d=4 x65,536 1.12 vs
+// 3.09, x20,467 0.81 vs 1.28, x4,096 0.43 vs 0.57.  At n = 6 / 8 the 255-register thread form loses (7.7 vs 7.4 ms
+// branch6, 13.3 vs 3.6 ms ncvx8).  TB_THREAD=0 forces the warp form.  Flop
+// counting stays in the warp kernel.
+inline bool thread_form(const KernelArgs& a, long long min_count) {
     if (a.flops || a.n != 4) return false;
     const char* e = getenv("TB_THREAD");
     if (e && e[0] == '0') return false;
     const char* m = getenv("TB_THREAD_MIN");
-    return a.count >= (m ? atoll(m) : 8192LL);
+    const long long total = a.route_count > a.count ? a.route_count : a.count;
+    return total >= (m ? atoll(m) : min_count);
 }
 
 template <int D, int FAM = TB_FAMILY_BRANCH>

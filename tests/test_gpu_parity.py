@@ -370,19 +370,30 @@ def test_extreme_scales_take_the_ieee_division_path(solver, d, h_scale, c_scale,
 
 
 # ---------------------------------------------------------------- thread form
-# n = 4 batches of >= TB_THREAD_MIN problems (default 8192) run one thread per
+# n = 4 batches of >= TB_THREAD_MIN problems (branch 4,096, ncvx 16,384) run one thread per
 # problem (csrc/tron_thread.cuh); these pin it to the oracle and to the warp
 # form (TB_THREAD=0), also on small batches forced through it (TB_THREAD_MIN=1).
 
 
-@pytest.mark.parametrize("fam", ["ncvx", "branch"])
-def test_thread_form_default_routing_bitwise(solver, monkeypatch, fam):
-    b = synth.make(fam, 16384, 4)
-    res = solver.solve_batch(b)  # >= 8192 problems: thread form
+@pytest.mark.parametrize("fam,count", [("ncvx", 16384), ("branch", 16384), ("branch", 20467)])
+def test_thread_form_default_routing_bitwise(solver, monkeypatch, fam, count):
+    b = synth.make(fam, count, 4)
+    res = solver.solve_batch(b)  # >= 16,384 / 4,096 problems (whole batch, any chunking): thread form
     ref = po.solve_batch(b, impl="oracle", workers=os.cpu_count() or 8)
     assert_bitwise(res, ref, label=f"{fam}4 thread form")
     monkeypatch.setenv("TB_THREAD", "0")
     assert_bitwise(solver.solve_batch(b), ref, label=f"{fam}4 warp form")
+    monkeypatch.delenv("TB_THREAD")
+    import torch
+
+    from paper_2106_14995_b200 import ProblemBatch, Solver
+
+    dev = torch.device("cuda", 0)
+    t = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(dev)  # noqa: E731
+    db = ProblemBatch(b.family, 4, t(b.lower), t(b.upper), t(b.params), t(b.x0))
+    out = Solver.alloc_result(count, 4, device=True)
+    solver.solve_batch(db, out=out)  # device-resident: concurrent chunks of the same batch
+    assert_bitwise(out, ref, label=f"{fam}4 thread form, device memspace")
 
 
 @pytest.mark.parametrize("cfg", [TronConfig(), TronConfig(max_iter=1), TronConfig(delta0=0.3), TronConfig(tol_pg=1e-9),
