@@ -52,8 +52,16 @@ extern "C" {
 #define TB_MEM_HOST 0
 #define TB_MEM_DEVICE 1
 
-#define TB_MODE_EXACT 0 /* reference op order, no FMA: bitwise parity */
-#define TB_MODE_FAST 1  /* FMA contraction + tree reductions (reports flips) */
+#define TB_MODE_EXACT 0 /* reference op order, no FMA: bitwise parity (the only mode) */
+
+/* Kernel form of a batch (tb_context_set_form).  Every form computes the same
+ * bits; the form only changes speed.  AUTO routes by family, dimension and
+ * batch size; the others force a form where it exists for the
+ * dimension (otherwise AUTO's choice is used). */
+#define TB_FORM_AUTO 0
+#define TB_FORM_WARP 1   /* one warp per problem, d <= 32 */
+#define TB_FORM_THREAD 3 /* one thread per problem, d = 4 */
+#define TB_FORM_BLOCK 4  /* 32 / 64 / 128 threads per problem, persistent, d >= 9 */
 
 /* TronConfig (tron.hpp:54-81), field for field; std::optional delta0 becomes
  * has_delta0 + delta0. */
@@ -125,9 +133,12 @@ int64_t tb_family_nparams(int32_t family, int32_t dim);
  * (batch.hpp:61-70). */
 int tb_context_create(const int32_t* devices, int32_t n_devices, tb_context** out);
 int tb_context_destroy(tb_context* ctx);
-/* TB_MODE_EXACT (default) or TB_MODE_FAST; fast_forward (default 1) skips the
- * provably identical replays of a rejected zero-change iteration. */
+/* mode must be TB_MODE_EXACT; fast_forward (default 1) skips the provably
+ * identical replays of a rejected zero-change iteration. */
 int tb_context_set_mode(tb_context* ctx, int32_t mode, int32_t fast_forward);
+/* Kernel form (TB_FORM_*, default TB_FORM_AUTO) for the context's later
+ * solves; replaces the round-1 TB_THREAD / TB_BLOCK_* environment switches. */
+int tb_context_set_form(tb_context* ctx, int32_t form);
 
 /* solve_batch (batch.hpp:27-78): blocking.  Returns TB_E_PROBLEM if any
  * problem reports a status >= TB_STATUS_EVALUATION_ERROR (the reference would

@@ -5,6 +5,7 @@ from .tron import (  # noqa: F401
     EvaluationError,
     Family,
     FactorizationError,
+    KernelForm,
     ImbalanceStats,
     ProblemBatch,
     SingularFactorError,

@@ -85,6 +85,7 @@ SIGNATURES = {
     "tb_context_create": (C.c_int, [C.POINTER(C.c_int32), C.c_int32, C.POINTER(C.c_void_p)]),
     "tb_context_destroy": (C.c_int, [C.c_void_p]),
     "tb_context_set_mode": (C.c_int, [C.c_void_p, C.c_int32, C.c_int32]),
+    "tb_context_set_form": (C.c_int, [C.c_void_p, C.c_int32]),
     "tb_solve_batch": (
         C.c_int,
         [C.c_void_p, C.POINTER(ProblemBatchC), C.POINTER(TronConfigC), C.POINTER(BatchResultC)],
@@ -125,6 +126,8 @@ def load() -> C.CDLL:
         )
     lib = C.CDLL(LIB_PATH)
     for name, (res, args) in SIGNATURES.items():
+        if os.environ.get("TB_LIB_PATH") and not hasattr(lib, name):
+            continue  # A/B experiments against an older library build
         fn = getattr(lib, name)
         fn.restype = res
         fn.argtypes = args

@@ -47,7 +47,13 @@ struct DevBuf {
     size_t cap = 0;
     cudaError_t ensure(size_t bytes) {
         if (bytes <= cap) return cudaSuccess;
-        if (p) cudaFree(p);
+        if (p) {
+            // work queued on any stream of this device may still use the old
+            // buffer (async solves): drain the device before releasing it
+            cudaError_t e = cudaDeviceSynchronize();
+            if (e != cudaSuccess) return e;
+            cudaFree(p);
+        }
         p = nullptr;
         cap = 0;
         cudaError_t e = cudaMalloc(&p, bytes);
@@ -70,7 +76,11 @@ struct DevState {
     DevBuf in;   // x0, lower, upper, params
     DevBuf out;  // results
     DevBuf flag;
-    DevBuf ws;   // block-kernel workspace (d > 32)
+    DevBuf ws;   // block-kernel workspace (d > 16)
+    // the last launch that used `ws` (block kernel): a later launch on any
+    // stream waits for it, so overlapping async solves never share the
+    // workspace's work counter and Hessian slices
+    cudaEvent_t ws_ev = nullptr;
 };
 
 __global__ void first_error_kernel(const int32_t* status, long long count, unsigned long long* out) {
@@ -84,6 +94,7 @@ struct tb_context {
     std::vector<DevState> devs;
     int mode = TB_MODE_EXACT;
     int fast_forward = 1;
+    int form = TB_FORM_AUTO;
 };
 
 extern "C" {
@@ -151,6 +162,7 @@ int tb_context_create(const int32_t* devices, int32_t n_devices, tb_context** ou
         for (int i = 0; i < 4 && e == cudaSuccess; ++i) e = cudaEventCreate(&d.ev[i]);
         if (e == cudaSuccess) e = cudaEventCreateWithFlags(&d.fork, cudaEventDisableTiming);
         if (e == cudaSuccess) e = cudaEventCreateWithFlags(&d.join, cudaEventDisableTiming);
+        if (e == cudaSuccess) e = cudaEventCreateWithFlags(&d.ws_ev, cudaEventDisableTiming);
         if (e != cudaSuccess) {
             ctx->devs.push_back(d);  // the partially created streams / events are released with it
             tb_context_destroy(ctx);
@@ -177,6 +189,7 @@ int tb_context_destroy(tb_context* ctx) {
             if (e) cudaEventDestroy(e);
         if (d.fork) cudaEventDestroy(d.fork);
         if (d.join) cudaEventDestroy(d.join);
+        if (d.ws_ev) cudaEventDestroy(d.ws_ev);
         if (d.stream) cudaStreamDestroy(d.stream);
         for (auto& a : d.aux)
             if (a) cudaStreamDestroy(a);
@@ -196,6 +209,14 @@ int tb_context_set_mode(tb_context* ctx, int32_t mode, int32_t fast_forward) {
         return set_err(TB_E_INVALID_ARGUMENT, "only TB_MODE_EXACT is built in this version");
     ctx->mode = mode;
     ctx->fast_forward = fast_forward ? 1 : 0;
+    return TB_OK;
+}
+
+int tb_context_set_form(tb_context* ctx, int32_t form) {
+    if (!ctx) return set_err(TB_E_INVALID_ARGUMENT, "null context");
+    if (form != TB_FORM_AUTO && form != TB_FORM_WARP && form != TB_FORM_THREAD && form != TB_FORM_BLOCK)
+        return set_err(TB_E_INVALID_ARGUMENT, "unknown kernel form %d", form);
+    ctx->form = form;
     return TB_OK;
 }
 
@@ -267,11 +288,14 @@ bool is_pinned(const void* p) {
 // e2e 7.18 / 7.45 / 7.54 / 7.58 / 7.95 / 8.11 M solves/s at 1 / 2 / 3 / 4 / 6 /
 // 8 chunks (smaller first H2D, finer copy/compute overlap); device-resident
 // 8.32 / 8.65 / 8.34 / 8.25 / 8.28 / 8.41 ms -> 4.
-constexpr int64_t kHostChunks = 8;
-constexpr int64_t kDeviceChunks = 4;
-int64_t max_chunks(bool host) {  // TB_CHUNKS overrides both (experiments); 1 disables the split
-    const char* e = std::getenv("TB_CHUNKS");
-    const int64_t v = e ? std::atoll(e) : (host ? kHostChunks : kDeviceChunks);
+#ifndef TB_HOST_CHUNKS
+#define TB_HOST_CHUNKS 8  // experiments: rebuild with -DTB_HOST_CHUNKS=k (1..8; 1 disables the split)
+#endif
+#ifndef TB_DEVICE_CHUNKS
+#define TB_DEVICE_CHUNKS 4
+#endif
+int64_t max_chunks(bool host) {
+    const int64_t v = host ? TB_HOST_CHUNKS : TB_DEVICE_CHUNKS;
     return v < 1 ? 1 : (v > 8 ? 8 : v);  // one stream per chunk: aux[8]
 }
 
@@ -311,7 +335,7 @@ const char* status_message(int st) {
     return "unknown";
 }
 
-tbdev::KernelArgs make_args(const tb_problem_batch* b, int64_t np, const tb_tron_config* cfg, int ff,
+tbdev::KernelArgs make_args(const tb_problem_batch* b, int64_t np, const tb_tron_config* cfg, int ff, int form,
                             const double* x0, const double* lo, const double* up, const double* prm,
                             int64_t stride, int64_t cnt, const OutPtrs& o) {
     tbdev::KernelArgs a;
@@ -338,18 +362,25 @@ tbdev::KernelArgs make_args(const tb_problem_batch* b, int64_t np, const tb_tron
     a.ws = nullptr;
     a.ws_bytes = 0;
     a.route_count = cnt;
+    a.next = nullptr;
+    a.form = form;
     return a;
 }
 
-// attach the block kernel's workspace (d > 32), grown on demand
-cudaError_t attach_ws(DevState& d, int family, tbdev::KernelArgs& a) {
+// attach the block kernel's workspace (d > 16), grown on demand; the launch
+// on `st` is ordered after the previous workspace user (ws_ev)
+cudaError_t attach_ws(DevState& d, int family, tbdev::KernelArgs& a, cudaStream_t st) {
     size_t need = 0;
-    cudaError_t e = tbdev::tron_ws_need(family, a.n, a.count, &need);
+    cudaError_t e = tbdev::tron_ws_need(family, a.n, a.count, a.form, &need);
     if (e != cudaSuccess || need == 0) return e;
     if ((e = d.ws.ensure(need)) != cudaSuccess) return e;
     a.ws = d.ws.p;
     a.ws_bytes = d.ws.cap;
-    return cudaSuccess;
+    return cudaStreamWaitEvent(st, d.ws_ev, 0);
+}
+// after a launch that used the workspace
+cudaError_t release_ws(DevState& d, const tbdev::KernelArgs& a, cudaStream_t st) {
+    return a.ws ? cudaEventRecord(d.ws_ev, st) : cudaSuccess;
 }
 
 // Device-resident batch on the warp kernel: `nch` concurrent chunk launches
@@ -387,12 +418,12 @@ cudaError_t launch_split(DevState& d, int family, const tbdev::KernelArgs& a, cu
     return e;
 }
 
-// chunk count of a device-resident batch (warp kernel only: the persistent
+// chunk count of a device-resident batch: only the one-shot warp kernel is
+// split (the persistent forms refill their groups from one counter; the
 // block kernel owns one workspace per device)
-int device_chunks(int family, int n, int64_t count) {
-    size_t need = 0;
-    if (tbdev::tron_ws_need(family, n, count, &need) != cudaSuccess || need != 0) return 1;
-    return count >= 2 * kChunkMin ? (int)std::min<int64_t>(max_chunks(false), count / kChunkMin) : 1;
+int device_chunks(const tbdev::KernelArgs& a, int family) {
+    if (tbdev::tron_form(family, a) != TB_FORM_WARP) return 1;
+    return a.count >= 2 * kChunkMin ? (int)std::min<int64_t>(max_chunks(false), a.count / kChunkMin) : 1;
 }
 
 }  // namespace
@@ -417,10 +448,11 @@ extern "C" int tb_solve_batch_async(tb_context* ctx, const tb_problem_batch* b, 
     cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : d.stream;
     OutPtrs o{r->x_star, r->f_star, r->pg_norm, r->status, r->iterations, r->cg_iterations, r->f_evals, r->flops,
               r->wall_time};
-    tbdev::KernelArgs a = make_args(b, np, cfg, ctx->fast_forward, b->x0, b->lower, b->upper, b->params,
+    tbdev::KernelArgs a = make_args(b, np, cfg, ctx->fast_forward, ctx->form, b->x0, b->lower, b->upper, b->params,
                                     b->params_stride, b->count, o);
-    CUDA_TRY(attach_ws(d, b->family, a));
-    CUDA_TRY(launch_split(d, b->family, a, st, device_chunks(b->family, b->dim, b->count)));
+    CUDA_TRY(attach_ws(d, b->family, a, st));
+    CUDA_TRY(launch_split(d, b->family, a, st, device_chunks(a, b->family)));
+    CUDA_TRY(release_ws(d, a, st));
     return TB_OK;
 }
 
@@ -475,7 +507,7 @@ extern "C" int tb_solve_batch(tb_context* ctx, const tb_problem_batch* b, const 
                                           (np == 0 || is_pinned(b->params)))) &&
                             (!out_host || (is_pinned(r->x_star) && is_pinned(r->f_star) && is_pinned(r->status)));
         size_t ws_need = 0;  // > 0: the persistent block kernel (one workspace per device): no chunking
-        CUDA_TRY(tbdev::tron_ws_need(b->family, n, c, &ws_need));
+        CUDA_TRY(tbdev::tron_ws_need(b->family, n, c, ctx->form, &ws_need));
         const int nch = (staged && ws_need == 0 && c >= 2 * kChunkMin)
                             ? (int)std::min<int64_t>(max_chunks(true), c / kChunkMin)
                             : 1;
@@ -529,12 +561,13 @@ extern "C" int tb_solve_batch(tb_context* ctx, const tb_problem_batch* b, const 
             OutPtrs o{off(ofull.x_star, n), off(ofull.f_star, 1), off(ofull.pg, 1), off(ofull.status, 1),
                       off(ofull.iters, 1), off(ofull.cg, 1),    off(ofull.fev, 1), off(ofull.flops, 1),
                       off(ofull.wall, 1)};
-            tbdev::KernelArgs a = make_args(b, np, cfg, ctx->fast_forward, x0, lw, up, prm, stride, cc, o);
+            tbdev::KernelArgs a = make_args(b, np, cfg, ctx->fast_forward, ctx->form, x0, lw, up, prm, stride, cc, o);
             a.route_count = c;  // kernel-form routing by the partition, not the pipeline chunk
-            CUDA_TRY(attach_ws(d, b->family, a));
+            CUDA_TRY(attach_ws(d, b->family, a, st));
             if (ch == 0) CUDA_TRY(cudaEventRecord(d.ev[1], st));
-            if (!staged) CUDA_TRY(launch_split(d, b->family, a, st, device_chunks(b->family, n, cc)));
+            if (!staged) CUDA_TRY(launch_split(d, b->family, a, st, device_chunks(a, b->family)));
             else CUDA_TRY(tbdev::launch_tron(b->family, a, st));
+            CUDA_TRY(release_ws(d, a, st));
             if (ch == nch - 1 && nch == 1) CUDA_TRY(cudaEventRecord(d.ev[2], st));
             if (out_host && cc > 0) {
                 const int64_t h0 = g0;

@@ -1126,8 +1126,12 @@ __global__ void __launch_bounds__(D, BlkMinBlocks<D>::value) tron_block_kernel(c
         double x = act ? a.x0[pid * n + t] : 0.0;
 
         // block-uniform loop state in shared memory, one copy per warp (warps
-        // run apart between barriers; inside a warp every lane stores the same
-        // value and reads its own store; registers set residency)
+        // run apart between barriers; registers set residency).  The counters
+        // (read-modify-write) are updated by lane 0 of each warp and read by
+        // thread 0; every lane stores the same value into the other slots, and
+        // f / delta_in / alpha_in, read by every lane before they are rewritten
+        // in the same pass, are rewritten after a __syncwarp
+        const bool wl0 = (t & 31) == 0;
         double* sc = W.misc + BM_SC + 8 * (t >> 5);
         long long& cg_iterations = reinterpret_cast<long long*>(sc)[0];
         long long& f_evals = reinterpret_cast<long long*>(sc)[1];
@@ -1162,7 +1166,7 @@ __global__ void __launch_bounds__(D, BlkMinBlocks<D>::value) tron_block_kernel(c
                 const double fe = fam.f(W);
                 TB_PH_END(W, 6)
                 W.count(tb_family_flops(FAM, n, 0));
-                ++f_evals;
+                if (wl0) ++f_evals;
                 bool take = iter == 0;
                 if (iter > 0) {
                     const double f_trial = fe;
@@ -1191,6 +1195,7 @@ __global__ void __launch_bounds__(D, BlkMinBlocks<D>::value) tron_block_kernel(c
                     take = actred > cfg.eta0 * prered;
                     if (take) {
                         x = xe;
+                        __syncwarp();  // every lane of the warp has read f
                         f = f_trial;
                         need_hessian = true;
                     }
@@ -1214,8 +1219,10 @@ __global__ void __launch_bounds__(D, BlkMinBlocks<D>::value) tron_block_kernel(c
                     if (delta <= 1e-300) break;
                     if (a.fast_forward && !take && iter >= 2 && delta == delta_in && alpha_c == alpha_in) {
                         const long long rem = cfg.max_iter - iter;
-                        cg_iterations += rem * cg_its;
-                        f_evals += rem;
+                        if (wl0) {
+                            cg_iterations += rem * cg_its;
+                            f_evals += rem;
+                        }
                         W.count(rem * (W.fl - fl_iter0));
                         iterations = cfg.max_iter;
                         break;
@@ -1231,6 +1238,7 @@ __global__ void __launch_bounds__(D, BlkMinBlocks<D>::value) tron_block_kernel(c
                     need_hessian = false;
                 }
                 fl_iter0 = W.fl;
+                __syncwarp();  // every lane of the warp has read delta_in / alpha_in
                 delta_in = delta;
                 alpha_in = alpha_c;
                 double cs, alpha_new;
@@ -1249,7 +1257,7 @@ __global__ void __launch_bounds__(D, BlkMinBlocks<D>::value) tron_block_kernel(c
                     status = rc;
                     break;
                 }
-                cg_iterations += cg_its;
+                if (wl0) cg_iterations += cg_its;
             }
         }
 #ifdef TB_PHASES

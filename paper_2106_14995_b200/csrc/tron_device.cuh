@@ -120,6 +120,10 @@ struct KernelArgs {
     // problems of the whole batch / partition this launch is a chunk of
     // (kernel-form routing, tron_thread.cuh thread_form); 0 = count
     long long route_count;
+    // persistent kernels (refilling thread form): problem counter, zeroed on
+    // the launch stream before the launch
+    unsigned long long* next;
+    int form;  // TB_FORM_* requested by the context (routing only)
 };
 
 // shared memory per warp (doubles; every region starts at an even offset)
@@ -989,10 +993,12 @@ __device__ __forceinline__ void tron_solve_one(const KernelArgs& a, const long l
     __syncwarp();
 
     // warp-uniform loop state in shared memory (registers are the residency
-    // limit, §4a).  All lanes execute these statements converged (warp-uniform
-    // conditions only, a __syncwarp in every staged reduction), so a
-    // read-modify-write such as ++f_evals reads the old value in every lane
-    // before any lane stores; the bitwise tests and the parity fuzz exercise it.
+    // limit, §4a).  The counters (read-modify-write) are updated and read by
+    // lane 0 alone.  The other slots take warp-uniform values that every lane
+    // stores identically; f, delta_in and alpha_in, which every lane reads
+    // before they are rewritten in the same pass, are rewritten only after a
+    // __syncwarp, so no lane can overwrite a value another lane has yet to
+    // read (independent thread scheduling).
     double* sc = smem + SL::SC;
     double& delta_in = sc[0];  // delta / alpha_c at the start of the iteration (zero-change check)
     double& alpha_in = sc[1];
@@ -1031,7 +1037,7 @@ __device__ __forceinline__ void tron_solve_one(const KernelArgs& a, const long l
             fam.prepare(W, xe);
             const double fe = fam.f(W);
             W.count(tb_family_flops(FAM, n, 0));
-            ++f_evals;
+            if (lane == 0) ++f_evals;
             TB_PH_END(W, 6)
             bool take = iter == 0;  // evaluate the gradient at xe
             if (iter > 0) {
@@ -1063,6 +1069,7 @@ __device__ __forceinline__ void tron_solve_one(const KernelArgs& a, const long l
                 take = actred > cfg.eta0 * prered;  // accepted (:529)
                 if (take) {
                     x = xe;
+                    __syncwarp();  // every lane has read f (actred, alphax)
                     f = f_trial;
                     need_hessian = true;
                 }
@@ -1091,8 +1098,10 @@ __device__ __forceinline__ void tron_solve_one(const KernelArgs& a, const long l
                 // exactly.  Fast-forward with identical counters.
                 if (a.fast_forward && !take && iter >= 2 && delta == delta_in && alpha_c == alpha_in) {
                     const long long rem = cfg.max_iter - iter;
-                    cg_iterations += rem * cg_its;
-                    f_evals += rem;
+                    if (lane == 0) {
+                        cg_iterations += rem * cg_its;
+                        f_evals += rem;
+                    }
                     W.count(rem * (W.fl - fl_iter0));
                     iterations = cfg.max_iter;
                     break;
@@ -1108,6 +1117,7 @@ __device__ __forceinline__ void tron_solve_one(const KernelArgs& a, const long l
                 need_hessian = false;
             }
             fl_iter0 = W.fl;
+            __syncwarp();  // every lane has read delta_in / alpha_in (zero-change test)
             delta_in = delta;
             alpha_in = alpha_c;
 
@@ -1127,7 +1137,7 @@ __device__ __forceinline__ void tron_solve_one(const KernelArgs& a, const long l
                 status = rc;  // FactorizationFailed caught like tron.hpp:499-501
                 break;
             }
-            cg_iterations += cg_its;
+            if (lane == 0) cg_iterations += cg_its;
         }
     }
 

@@ -9,6 +9,7 @@
 #include "tron_block.cuh"
 #include "tron_device.cuh"
 #include "tron_launch.h"
+#include "tron_thread.cuh"
 
 namespace tbdev {
 
@@ -31,14 +32,13 @@ static cudaError_t launch_fd(const KernelArgs& a, cudaStream_t st) {
     return a.flops ? launch_fdc<FAM, D, true>(a, st) : launch_fdc<FAM, D, false>(a, st);
 }
 
-// ---------------------------------------------------------------- d > 32
-// Hessian placement of the block kernel: TB_BLOCK_ASMEM=1 keeps A in shared
-// memory (fewer resident problems per SM), default 0 keeps it in the
-// L2-resident global workspace.
-inline bool blk_asmem() {
-    const char* e = std::getenv("TB_BLOCK_ASMEM");
-    return e && e[0] == '1';
-}
+// ---------------------------------------------------------------- d > 16
+// Hessian placement of the block kernel: compile with -DTB_BLOCK_ASMEM=1 to
+// keep A in shared memory (fewer resident problems per SM; experiments), the
+// default keeps it in the L2-resident global workspace.
+#ifndef TB_BLOCK_ASMEM
+#define TB_BLOCK_ASMEM 0
+#endif
 
 // Dimension routing (ncvx, B = 32,768, device-resident, ms):
 //   d        12     16     17..20        24     32
@@ -47,16 +47,13 @@ inline bool blk_asmem() {
 //   blk64  14.85  19.28  ~/ 25.22      30.19  50.10
 // so d <= 16 runs the warp kernel, 17..32 the one-warp D = 32 block kernel
 // (compacted systems, 8/16-lane lockstep attempt groups), 33..64 D = 64 and
-// 65..128 D = 128.  TB_BLOCK_MIN_DIM (9..33) and TB_BLOCK32=0 override.
-inline int blk_min_dim() {
-    const char* e = std::getenv("TB_BLOCK_MIN_DIM");
-    const int v = e ? std::atoi(e) : 17;
-    return v < 9 ? 9 : v;
+// 65..128 D = 128.  TB_FORM_WARP keeps d = 17..32 on the D = 32 warp kernel,
+// TB_FORM_BLOCK moves d = 9..16 to the block kernel.
+inline bool use_block(int n, int form) {
+    if (n >= 17) return !(form == TB_FORM_WARP && n <= 32);
+    return form == TB_FORM_BLOCK && n >= 9;
 }
-inline bool blk32() {
-    const char* e = std::getenv("TB_BLOCK32");
-    return !(e && e[0] == '0');
-}
+inline int block_dim(int n) { return n <= 32 ? 32 : (n <= 64 ? 64 : 128); }
 
 // persistent grid: resident blocks per SM x SMs, capped by the batch
 template <int FAM, int D, bool ASMEM, bool COUNT>
@@ -94,9 +91,8 @@ static cudaError_t launch_blk_c(const KernelArgs& a, cudaStream_t st) {
 
 template <int FAM, int D>
 static cudaError_t launch_blk(const KernelArgs& a, cudaStream_t st) {
-    if (blk_asmem())
-        return a.flops ? launch_blk_c<FAM, D, true, true>(a, st) : launch_blk_c<FAM, D, true, false>(a, st);
-    return a.flops ? launch_blk_c<FAM, D, false, true>(a, st) : launch_blk_c<FAM, D, false, false>(a, st);
+    constexpr bool AS = TB_BLOCK_ASMEM != 0;
+    return a.flops ? launch_blk_c<FAM, D, AS, true>(a, st) : launch_blk_c<FAM, D, AS, false>(a, st);
 }
 
 // workspace bytes the block kernel needs for `count` problems of dim n
@@ -105,19 +101,71 @@ static cudaError_t ws_need_blk(long long count, size_t* bytes) {
     long long grid = 0;
     size_t smem = 0;
     *bytes = kBlkWsHeader;
-    const bool as = blk_asmem();
-    cudaError_t e = as ? blk_grid<FAM, D, true, false>(count, &grid, &smem)
-                       : blk_grid<FAM, D, false, false>(count, &grid, &smem);
+    constexpr bool as = TB_BLOCK_ASMEM != 0;
+    cudaError_t e = blk_grid<FAM, D, as, false>(count, &grid, &smem);
     if (e != cudaSuccess) return e;
     long long g2 = 0;
-    if ((e = as ? blk_grid<FAM, D, true, true>(count, &g2, &smem) : blk_grid<FAM, D, false, true>(count, &g2, &smem)) !=
-        cudaSuccess)
-        return e;
+    if ((e = blk_grid<FAM, D, as, true>(count, &g2, &smem)) != cudaSuccess) return e;
     if (g2 > grid) grid = g2;
     using SL = BlkLayout<D, false>;
     if (!as) *bytes += sizeof(double) * (size_t)grid * D * D;
     if (SL::LP < SL::LPFULL) *bytes += sizeof(double) * (size_t)grid * SL::LPFULL;
     return cudaSuccess;
+}
+
+// ---------------------------------------------------------------- routing
+// n = 4 without flop counting: TB_FORM_THREAD, or TB_FORM_AUTO on batches
+// (the whole batch / partition, not the pipeline chunk) of >= min_count
+inline bool thread_form(const KernelArgs& a, long long min_count) {
+    if (a.flops || a.n != 4 || min_count < 0) return false;
+    if (a.form == TB_FORM_THREAD) return true;
+    if (a.form != TB_FORM_AUTO) return false;
+    const long long total = a.route_count > a.count ? a.route_count : a.count;
+    return total >= min_count;
+}
+
+// the one routing decision (launchers and tron_form): block kernel for large
+// d, thread form for big n = 4 batches of the families that have it (branch
+// from 4,096 problems, ncvx from 16,384), the warp kernel
+// otherwise
+inline int resolve_form(int family, const KernelArgs& a) {
+    if (family != TB_FAMILY_BRANCH && use_block(a.n, a.form)) return TB_FORM_BLOCK;
+    const long long min_thread = family == TB_FAMILY_BRANCH ? 4096 : (family == TB_FAMILY_NCVX ? 16384 : -1);
+    if (thread_form(a, min_thread)) return TB_FORM_THREAD;
+    return TB_FORM_WARP;
+}
+
+// hs45 / boxqp / ncvx: D = next of {4, 8, 16, 32} >= dim on the warp form,
+// the block kernel above (use_block)
+template <int FAM>
+static cudaError_t launch_family(const KernelArgs& a, cudaStream_t st) {
+    const int n = a.n;
+    switch (resolve_form(FAM, a)) {
+        case TB_FORM_BLOCK: {
+            const int D = block_dim(n);
+            if (D == 32) return launch_blk<FAM, 32>(a, st);
+            if (D == 64) return launch_blk<FAM, 64>(a, st);
+            return launch_blk<FAM, 128>(a, st);
+        }
+        case TB_FORM_THREAD:
+            if constexpr (FAM == TB_FAMILY_NCVX) return launch_thread<4, FAM>(a, st);
+            return cudaErrorInvalidValue;
+    }
+    if (n <= 4) return launch_fd<FAM, 4>(a, st);
+    if (n <= 8) return launch_fd<FAM, 8>(a, st);
+    if (n <= 16) return launch_fd<FAM, 16>(a, st);
+    return launch_fd<FAM, 32>(a, st);
+}
+
+// workspace bytes the block kernel needs (0: another form)
+template <int FAM>
+static cudaError_t family_ws_need(int n, long long count, int form, size_t* bytes) {
+    *bytes = 0;
+    if (FAM == TB_FAMILY_BRANCH || !use_block(n, form)) return cudaSuccess;
+    const int D = block_dim(n);
+    if (D == 32) return ws_need_blk<FAM, 32>(count, bytes);
+    if (D == 64) return ws_need_blk<FAM, 64>(count, bytes);
+    return ws_need_blk<FAM, 128>(count, bytes);
 }
 
 }  // namespace tbdev

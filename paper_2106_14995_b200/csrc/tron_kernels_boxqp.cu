@@ -1,25 +1,11 @@
 // tron_kernels_boxqp.cu — TB_FAMILY_BOXQP kernels: D = next of {4, 8, 16, 32} >= dim (one warp per
-// problem) up to d = 16; above it the block kernel with D = 32, 64 or 128 threads (tron_kernels.cuh).
+// problem) up to d = 16; above it the block kernel (tron_kernels.cuh).
 #include "tron_kernels.cuh"
 
 namespace tbdev {
-cudaError_t launch_boxqp(const KernelArgs& a, cudaStream_t st) {
-    if (a.n <= 4) return launch_fd<TB_FAMILY_BOXQP, 4>(a, st);
-    if (a.n <= 8) return launch_fd<TB_FAMILY_BOXQP, 8>(a, st);
-    if (a.n >= blk_min_dim()) {
-        if (a.n <= 32 && blk32()) return launch_blk<TB_FAMILY_BOXQP, 32>(a, st);
-        if (a.n <= 64) return launch_blk<TB_FAMILY_BOXQP, 64>(a, st);
-        return launch_blk<TB_FAMILY_BOXQP, 128>(a, st);
-    }
-    if (a.n <= 16) return launch_fd<TB_FAMILY_BOXQP, 16>(a, st);
-    return launch_fd<TB_FAMILY_BOXQP, 32>(a, st);
-}
-cudaError_t ws_need_boxqp(int n, long long count, size_t* bytes) {
-    *bytes = 0;
-    if (n <= 8 || n < blk_min_dim()) return cudaSuccess;
-    if (n <= 32 && blk32()) return ws_need_blk<TB_FAMILY_BOXQP, 32>(count, bytes);
-    if (n <= 64) return ws_need_blk<TB_FAMILY_BOXQP, 64>(count, bytes);
-    return ws_need_blk<TB_FAMILY_BOXQP, 128>(count, bytes);
+cudaError_t launch_boxqp(const KernelArgs& a, cudaStream_t st) { return launch_family<TB_FAMILY_BOXQP>(a, st); }
+cudaError_t ws_need_boxqp(int n, long long count, int form, size_t* bytes) {
+    return family_ws_need<TB_FAMILY_BOXQP>(n, count, form, bytes);
 }
 }  // namespace tbdev
 

@@ -1,12 +1,13 @@
 // tron_kernels_branch.cu — ADMM branch family kernels, D = dim exactly (4, 6).
 #include "tron_kernels.cuh"
-#include "tron_thread.cuh"
 
 namespace tbdev {
+// D = dim exactly (4 or 6): thread form (n = 4, large batches) or warp form
 cudaError_t launch_branch(const KernelArgs& a, cudaStream_t st) {
-    if (thread_form(a, 4096)) return launch_thread<4, TB_FAMILY_BRANCH>(a, st);
-    if (a.n == 4) return launch_fd<TB_FAMILY_BRANCH, 4>(a, st);
-    return launch_fd<TB_FAMILY_BRANCH, 6>(a, st);
+    switch (resolve_form(TB_FAMILY_BRANCH, a)) {
+        case TB_FORM_THREAD: return launch_thread<4, TB_FAMILY_BRANCH>(a, st);
+    }
+    return a.n == 4 ? launch_fd<TB_FAMILY_BRANCH, 4>(a, st) : launch_fd<TB_FAMILY_BRANCH, 6>(a, st);
 }
 }  // namespace tbdev
 

@@ -4,24 +4,9 @@
 #include "tron_thread.cuh"
 
 namespace tbdev {
-cudaError_t launch_ncvx(const KernelArgs& a, cudaStream_t st) {
-    if (thread_form(a, 16384)) return launch_thread<4, TB_FAMILY_NCVX>(a, st);
-    if (a.n <= 4) return launch_fd<TB_FAMILY_NCVX, 4>(a, st);
-    if (a.n <= 8) return launch_fd<TB_FAMILY_NCVX, 8>(a, st);
-    if (a.n >= blk_min_dim()) {
-        if (a.n <= 32 && blk32()) return launch_blk<TB_FAMILY_NCVX, 32>(a, st);
-        if (a.n <= 64) return launch_blk<TB_FAMILY_NCVX, 64>(a, st);
-        return launch_blk<TB_FAMILY_NCVX, 128>(a, st);
-    }
-    if (a.n <= 16) return launch_fd<TB_FAMILY_NCVX, 16>(a, st);
-    return launch_fd<TB_FAMILY_NCVX, 32>(a, st);
-}
-cudaError_t ws_need_ncvx(int n, long long count, size_t* bytes) {
-    *bytes = 0;
-    if (n <= 8 || n < blk_min_dim()) return cudaSuccess;
-    if (n <= 32 && blk32()) return ws_need_blk<TB_FAMILY_NCVX, 32>(count, bytes);
-    if (n <= 64) return ws_need_blk<TB_FAMILY_NCVX, 64>(count, bytes);
-    return ws_need_blk<TB_FAMILY_NCVX, 128>(count, bytes);
+cudaError_t launch_ncvx(const KernelArgs& a, cudaStream_t st) { return launch_family<TB_FAMILY_NCVX>(a, st); }
+cudaError_t ws_need_ncvx(int n, long long count, int form, size_t* bytes) {
+    return family_ws_need<TB_FAMILY_NCVX>(n, count, form, bytes);
 }
 }  // namespace tbdev
 

@@ -9,9 +9,14 @@ struct KernelArgs;
 namespace tbdev {
 cudaError_t launch_tron(int family, const KernelArgs& a, cudaStream_t st);
 int max_warp_dim();
+// the TB_FORM_* launch_tron resolves `a` to (never TB_FORM_AUTO)
+int tron_form(int family, const KernelArgs& a);
 int max_dim();
-cudaError_t tron_ws_need(int family, int n, long long count, size_t* bytes);
+cudaError_t tron_ws_need(int family, int n, long long count, int form, size_t* bytes);
 // kernels of this library launched so far (TRON phases, ADMM stages)
 void note_launches(long long k);
+// a problem-counter slot on the current device for one persistent launch
+// (round-robin over a pool; the launcher zeroes it on its stream)
+cudaError_t counter_slot(unsigned long long** out);
 long long launches();
 }  // namespace tbdev

@@ -667,15 +667,6 @@ __device__ __forceinline__ void tron_solve_thread(const KernelArgs& a, const lon
 // 3.09, x20,467 0.81 vs 1.28, x4,096 0.43 vs 0.57.  At n = 6 / 8 the 255-register thread form loses (7.7 vs 7.4 ms
 // branch6, 13.3 vs 3.6 ms ncvx8).  TB_THREAD=0 forces the warp form.  Flop
 // counting stays in the warp kernel.
-inline bool thread_form(const KernelArgs& a, long long min_count) {
-    if (a.flops || a.n != 4) return false;
-    const char* e = getenv("TB_THREAD");
-    if (e && e[0] == '0') return false;
-    const char* m = getenv("TB_THREAD_MIN");
-    const long long total = a.route_count > a.count ? a.route_count : a.count;
-    return total >= (m ? atoll(m) : min_count);
-}
-
 template <int D, int FAM = TB_FAMILY_BRANCH>
 __global__ void __launch_bounds__(64) tron_thread_kernel(const __grid_constant__ KernelArgs a) {
     const long long pid = blockIdx.x * (long long)blockDim.x + threadIdx.x;

@@ -63,6 +63,16 @@ class Family(enum.IntEnum):
     BRANCH = L.TB_FAMILY_BRANCH
 
 
+class KernelForm(enum.IntEnum):
+    """tb_capi.h TB_FORM_*: which device kernel form solves a batch.  Every
+    form returns the same bits; AUTO routes by family, dimension and size."""
+
+    AUTO = 0
+    WARP = 1    # one warp per problem (d <= 32)
+    THREAD = 3  # one thread per problem (d = 4)
+    BLOCK = 4   # 32 / 64 / 128 threads per problem, persistent (d >= 9)
+
+
 @dataclass
 class TronConfig:
     """tron.hpp:54-81, same defaults."""
@@ -184,7 +194,8 @@ class Solver:
     """Owns a tb_context (device streams + workspace).  `devices` plays the
     role of solve_batch's `workers`: contiguous even partitions per device."""
 
-    def __init__(self, devices: Sequence[int] = (0,), fast_forward: bool = True):
+    def __init__(self, devices: Sequence[int] = (0,), fast_forward: bool = True,
+                 form: "KernelForm" = KernelForm.AUTO):
         self._lib = L.load()
         arr = (C.c_int32 * len(devices))(*devices)
         ctx = C.c_void_p()
@@ -194,6 +205,16 @@ class Solver:
         self.devices = list(devices)
         if self._lib.tb_context_set_mode(self._ctx, 0, 1 if fast_forward else 0) != L.TB_OK:
             raise SolverError(L.last_error())
+        self.set_form(form)
+
+    def set_form(self, form: "KernelForm") -> None:
+        """Kernel form of later solves (TB_FORM_*; results are identical)."""
+        if int(form) == 0 and not hasattr(self._lib, "tb_context_set_form"):
+            self.form = KernelForm.AUTO  # older library build (A/B experiments)
+            return
+        if self._lib.tb_context_set_form(self._ctx, int(form)) != L.TB_OK:
+            raise ValueError(L.last_error())
+        self.form = KernelForm(int(form))
 
     def close(self) -> None:
         if getattr(self, "_ctx", None):
@@ -216,6 +237,16 @@ class Solver:
             raise ValueError("solve_batch: no starting points")
         dev = _is_device(problems.lower)
         n, N = int(problems.dim), problems.count
+        # every input array must live where `lower` lives (a host pointer
+        # passed as device memory would fault and poison the CUDA context)
+        for name, arr in (("x0s", x0s), ("upper", problems.upper), ("params", problems.params)):
+            if arr is None:
+                continue
+            if _is_device(arr) != dev:
+                raise ValueError(f"solve_batch: {name} is in {'device' if _is_device(arr) else 'host'} memory "
+                                 f"but lower is in {'device' if dev else 'host'} memory")
+            if dev and arr.device != problems.lower.device:
+                raise ValueError(f"solve_batch: {name} is on {arr.device}, lower on {problems.lower.device}")
         if not dev:
             x0s = _host_f64(x0s)
             lower, upper = _host_f64(problems.lower), _host_f64(problems.upper)

@@ -1,3 +1,4 @@
+import contextlib
 import os
 import sys
 
@@ -34,6 +35,18 @@ def assert_bitwise(res, ref, fields=FIELDS, label=""):
             i = int(np.argmin(eqp))
             raise AssertionError(f"{label}: field {k} differs at problem {i}: {a[i]!r} vs {b[i]!r} "
                                  f"({int((~eqp).sum())} problems differ)")
+
+
+@contextlib.contextmanager
+def forced_form(solver, form):
+    """Run the block with the session solver forced to a kernel form."""
+    from paper_2106_14995_b200 import KernelForm
+
+    solver.set_form(form)
+    try:
+        yield solver
+    finally:
+        solver.set_form(KernelForm.AUTO)
 
 
 @pytest.fixture(scope="session")

@@ -3,9 +3,9 @@ same seeded inputs.  Exact mode is bit-identical for every SolveReport field."""
 import numpy as np
 import pytest
 
-from conftest import assert_bitwise, host
+from conftest import assert_bitwise, forced_form, host
 from oracle import pyoracle as po
-from paper_2106_14995_b200 import SolveStatus, TronConfig, synth
+from paper_2106_14995_b200 import KernelForm, SolveStatus, TronConfig, synth
 
 pytestmark = pytest.mark.gpu
 
@@ -207,13 +207,11 @@ def test_dimension_over_device_capacity_rejected(solver):
 
 
 # ------------------------------------------------- d > 32: the block kernel
-@pytest.mark.parametrize("asmem", ["0", "1"])
 @pytest.mark.parametrize("d", [17, 24, 32, 33, 40, 64, 65, 100, 128])
-def test_block_kernel_ncvx_bitwise(solver, monkeypatch, d, asmem):
+def test_block_kernel_ncvx_bitwise(solver, d):
     """C3 sweep on the block kernel: D = 32 / 64 / 128 threads per problem, Hessian in
-    the global workspace (default) or in shared memory (TB_BLOCK_ASMEM=1);
-    every field, and the flop counters, bit-identical to the oracle."""
-    monkeypatch.setenv("TB_BLOCK_ASMEM", asmem)
+    the global workspace; every field, and the flop counters, bit-identical to the oracle."""
+    asmem = "0"
     n = 48 if d <= 64 else 16
     b = synth.ncvx(n, d, seed=3 + d)
     res = solver.solve_batch(b, count_flops=True)
@@ -370,9 +368,10 @@ def test_extreme_scales_take_the_ieee_division_path(solver, d, h_scale, c_scale,
 
 
 # ---------------------------------------------------------------- thread form
-# n = 4 batches of >= TB_THREAD_MIN problems (branch 4,096, ncvx 16,384) run one thread per
+# n = 4 batches of >= 4,096 (branch) / 16,384 (ncvx) problems run one thread per
 # problem (csrc/tron_thread.cuh); these pin it to the oracle and to the warp
-# form (TB_THREAD=0), also on small batches forced through it (TB_THREAD_MIN=1).
+# form (KernelForm.WARP), also on small batches forced through it
+# (KernelForm.THREAD).
 
 
 @pytest.mark.parametrize("fam,count", [("ncvx", 16384), ("branch", 16384), ("branch", 20467)])
@@ -381,9 +380,9 @@ def test_thread_form_default_routing_bitwise(solver, monkeypatch, fam, count):
     res = solver.solve_batch(b)  # >= 16,384 / 4,096 problems (whole batch, any chunking): thread form
     ref = po.solve_batch(b, impl="oracle", workers=os.cpu_count() or 8)
     assert_bitwise(res, ref, label=f"{fam}4 thread form")
-    monkeypatch.setenv("TB_THREAD", "0")
-    assert_bitwise(solver.solve_batch(b), ref, label=f"{fam}4 warp form")
-    monkeypatch.delenv("TB_THREAD")
+    for form in (KernelForm.WARP,):
+        with forced_form(solver, form):
+            assert_bitwise(solver.solve_batch(b), ref, label=f"{fam}4 {form.name} form")
     import torch
 
     from paper_2106_14995_b200 import ProblemBatch, Solver
@@ -399,15 +398,20 @@ def test_thread_form_default_routing_bitwise(solver, monkeypatch, fam, count):
 @pytest.mark.parametrize("cfg", [TronConfig(), TronConfig(max_iter=1), TronConfig(delta0=0.3), TronConfig(tol_pg=1e-9),
                                  TronConfig(cg_tol=0.5, mu0=0.1, interp_factor=0.25),
                                  TronConfig(sigma1=0.1, sigma2=0.3, sigma3=2.0, eta0=0.01, delta_max=5.0)])
-def test_thread_form_config_variants_bitwise(solver, monkeypatch, cfg):
-    monkeypatch.setenv("TB_THREAD_MIN", "1")
-    for b in (synth.ncvx(300, 4, seed=9), synth.branch(300, 4, seed=9)):
-        assert_bitwise(solver.solve_batch(b, cfg=cfg), po.solve_batch(b, cfg=cfg, impl="oracle"),
-                       label=f"thread form {cfg}")
+def test_thread_form_config_variants_bitwise(solver, cfg):
+    with forced_form(solver, KernelForm.THREAD):
+        for b in (synth.ncvx(300, 4, seed=9), synth.branch(300, 4, seed=9)):
+            assert_bitwise(solver.solve_batch(b, cfg=cfg), po.solve_batch(b, cfg=cfg, impl="oracle"),
+                           label=f"thread form {cfg}")
 
 
-def test_thread_form_outside_box_infinite_bounds_and_bad_bounds(solver, monkeypatch):
-    monkeypatch.setenv("TB_THREAD_MIN", "1")
+@pytest.mark.parametrize("form", ["THREAD", "WARP"])
+def test_small_forms_outside_box_infinite_bounds_and_bad_bounds(solver, form):
+    with forced_form(solver, KernelForm[form]):
+        _outside_box_inf_bad_bounds(solver)
+
+
+def _outside_box_inf_bad_bounds(solver):
     b = synth.ncvx(200, 4, seed=11)
     b.lower[::3, 1] = -np.inf
     b.upper[::4, 2] = np.inf
@@ -421,19 +425,24 @@ def test_thread_form_outside_box_infinite_bounds_and_bad_bounds(solver, monkeypa
         solver.solve_batch(b)
 
 
-def test_thread_form_ragged_counts_and_device_memspace(solver, monkeypatch):
+@pytest.mark.parametrize("form", ["THREAD", "WARP"])
+def test_small_forms_ragged_counts_and_device_memspace(solver, form):
+    with forced_form(solver, KernelForm[form]):
+        _ragged_device(solver, form)
+
+
+def _ragged_device(solver, form):
     import torch
 
     from paper_2106_14995_b200 import ProblemBatch, Solver
 
-    monkeypatch.setenv("TB_THREAD_MIN", "1")
     for n in (1, 63, 64, 65, 129):
         b = synth.ncvx(n, 4, seed=20 + n)
-        assert_bitwise(solver.solve_batch(b), po.solve_batch(b, impl="oracle"), label=f"thread form n={n}")
+        assert_bitwise(solver.solve_batch(b), po.solve_batch(b, impl="oracle"), label=f"{form} form n={n}")
     b = synth.branch(1000, 4, seed=3)
     dev = torch.device("cuda", 0)
     t = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(dev)  # noqa: E731
     db = ProblemBatch(b.family, 4, t(b.lower), t(b.upper), t(b.params), t(b.x0))
     out = Solver.alloc_result(1000, 4, device=True)
     solver.solve_batch(db, out=out)
-    assert_bitwise(out, po.solve_batch(b, impl="oracle"), label="thread form device memspace")
+    assert_bitwise(out, po.solve_batch(b, impl="oracle"), label=f"{form} form device memspace")
