@@ -174,7 +174,9 @@ int tb_measure_fp64_peak(int32_t device, double* tflops);
  * tb_admm_solve_components the caller all-gathers the branch solutions (NCCL)
  * into the buffer of tb_admm_branch_solution, then tb_admm_update_consensus
  * runs the bus / multiplier / residual step and leaves this shard's residual
- * maxima for a max-allreduce.  Single process: tb_admm_step. */
+ * maxima (and branch-failure flag) for a max-allreduce.  Single process:
+ * tb_admm_step, or tb_admm_run for a whole solve without per-iteration host
+ * round trips. */
 typedef struct tb_admm_grid {
     int32_t n_bus, n_gen, n_branch;
     const double *bus_pd, *bus_qd, *bus_gsh, *bus_bsh, *bus_vmin, *bus_vmax; /* [n_bus], per unit */
@@ -205,6 +207,10 @@ typedef struct tb_admm_options {
     double auglag_xi_max;    /* default 1e8 */
     double auglag_eta0;      /* default 0.1 */
     double auglag_feas_tol;  /* default 1e-6 */
+    /* d = 4 branch stage: TB_FORM_AUTO (one thread per branch, launched
+     * together with the generator updates) or TB_FORM_WARP (one warp per
+     * branch); results are identical */
+    int32_t branch_form;
 } tb_admm_options;
 
 typedef struct tb_admm tb_admm;
@@ -223,6 +229,9 @@ typedef struct tb_admm tb_admm;
 #define TB_ADMM_COST 11 /* sum_g c2 p^2 + c1 p */
 #define TB_ADMM_AUGLAG_ROUNDS 12 /* int64 [1]: AL rounds run so far (line_limits) */
 #define TB_ADMM_LINE_VIOL 13     /* double [1]: max over branches and ends of |h| (line_limits) */
+#define TB_ADMM_STAGE_TIMES 14   /* double [2]: seconds of the latest iteration's components (generators +
+                                    branch TRON) and consensus stages, device events (per-partition batch
+                                    time of SPEC.md:408) */
 
 void tb_admm_options_default(tb_admm_options* opt);
 /* x_external: optional device buffer for the branch solutions,
@@ -232,8 +241,23 @@ int tb_admm_create(const tb_admm_grid* grid, const tb_admm_options* opt, int32_t
 int tb_admm_destroy(tb_admm* a);
 int tb_admm_solve_components(tb_admm* a, void* stream);
 int tb_admm_branch_solution(tb_admm* a, double** x_dev, int64_t* lo, int64_t* hi);
-int tb_admm_update_consensus(tb_admm* a, void* stream, double* res2_dev);
+/* res3_dev (device, 3 doubles, may be NULL): this shard's residual maxima and
+ * its first failed branch (-1 none) -- max-allreduce them across shards. */
+int tb_admm_update_consensus(tb_admm* a, void* stream, double* res3_dev);
+/* One iteration, blocking: residuals to host.  TB_E_PROBLEM when a branch
+ * solve ended where the reference throws ("propagated solver
+ * failures"); the message names the branch and status. */
 int tb_admm_step(tb_admm* a, double* primal, double* dual);
+/* admm_solve, single shard: up to max_iter iterations, stop
+ * at the first whose residuals are both <= tol; one captured CUDA graph per
+ * iteration, a device stop flag, the host polls every check_every
+ * iterations (no per-iteration round trip).  hist_out [max_iter][2] (NULL
+ * allowed), *iters_out = iterations run.  TB_E_PROBLEM as tb_admm_step. */
+int tb_admm_run(tb_admm* a, int32_t max_iter, double tol_primal, double tol_dual, int32_t check_every,
+                double* hist_out, int32_t* iters_out);
+/* Sharded path: first failed branch (global index, -1 none) since the last
+ * call and its status; blocking; clears the record. */
+int tb_admm_branch_errors(tb_admm* a, int64_t* first_bad, int32_t* status);
 int tb_admm_get(tb_admm* a, int32_t what, void* host_out);
 const char* tb_admm_last_error(void);
 

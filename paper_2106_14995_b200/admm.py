@@ -21,7 +21,8 @@ from .tron import SolverError, TronConfig
 
 GEN_P, GEN_Q, GEN_PT, GEN_QT, GEN_LP, GEN_LQ, BUS_WT, BUS_TT = range(8)
 BRANCH_X, BRANCH_PARAMS, BRANCH_STATUS, COST = 8, 9, 10, 11
-AUGLAG_ROUNDS, LINE_VIOL = 12, 13
+AUGLAG_ROUNDS, LINE_VIOL, STAGE_TIMES = 12, 13, 14
+TB_E_PROBLEM = 4
 
 
 @dataclass
@@ -85,7 +86,7 @@ class OptionsC(C.Structure):
     _fields_ = [("rho_pq", C.c_double), ("rho_va", C.c_double), ("shard_rank", C.c_int32),
                 ("shard_count", C.c_int32), ("tron", L.TronConfigC), ("line_limits", C.c_int32),
                 ("auglag_max_iter", C.c_int32), ("auglag_xi0", C.c_double), ("auglag_xi_max", C.c_double),
-                ("auglag_eta0", C.c_double), ("auglag_feas_tol", C.c_double)]
+                ("auglag_eta0", C.c_double), ("auglag_feas_tol", C.c_double), ("branch_form", C.c_int32)]
 
 
 @dataclass
@@ -101,6 +102,9 @@ class AdmmOptions:
     auglag_xi_max: float = 1e8
     auglag_eta0: float = 0.1
     auglag_feas_tol: float = 1e-6
+    # d = 4 branch stage kernel form: "auto" (thread per branch, fused with the
+    # generator updates) or "warp" (warp per branch); identical results
+    branch_form: str = "auto"
 
     @property
     def branch_dim(self) -> int:
@@ -114,6 +118,7 @@ class AdmmOptions:
         o.auglag_max_iter = self.auglag_max_iter
         o.auglag_xi0, o.auglag_xi_max = self.auglag_xi0, self.auglag_xi_max
         o.auglag_eta0, o.auglag_feas_tol = self.auglag_eta0, self.auglag_feas_tol
+        o.branch_form = {"auto": 0, "warp": 1}[self.branch_form]
         return o
 
 
@@ -124,6 +129,9 @@ _SIG = {
     "tb_admm_branch_solution": (C.c_int, [C.c_void_p, C.POINTER(C.c_void_p), C.POINTER(C.c_int64), C.POINTER(C.c_int64)]),
     "tb_admm_update_consensus": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p]),
     "tb_admm_step": (C.c_int, [C.c_void_p, C.POINTER(C.c_double), C.POINTER(C.c_double)]),
+    "tb_admm_run": (C.c_int, [C.c_void_p, C.c_int32, C.c_double, C.c_double, C.c_int32, C.c_void_p,
+                              C.POINTER(C.c_int32)]),
+    "tb_admm_branch_errors": (C.c_int, [C.c_void_p, C.POINTER(C.c_int64), C.POINTER(C.c_int32)]),
     "tb_admm_get": (C.c_int, [C.c_void_p, C.c_int32, C.c_void_p]),
     "tb_admm_last_error": (C.c_char_p, []),
     "tb_admm_options_default": (None, [C.POINTER(OptionsC)]),
@@ -167,22 +175,43 @@ class AdmmSolver:
 
     def _check(self, rc):
         if rc != 0:
-            raise SolverError(self.lib.tb_admm_last_error().decode())
+            raise _admm_error(rc, self.lib.tb_admm_last_error().decode())
 
     def step(self) -> Tuple[float, float]:
-        """One ADMM iteration (single process): returns (primal, dual)."""
+        """One ADMM iteration (single process): returns (primal, dual).  A
+        branch solve that ends where the reference throws raises its
+        exception type (solver failures propagate)."""
         p, d = C.c_double(), C.c_double()
         self._check(self.lib.tb_admm_step(self._h, C.byref(p), C.byref(d)))
         self.history.append((p.value, d.value))
         return p.value, d.value
 
-    def run(self, max_iter: int, tol_primal: float = 0.0, tol_dual: float = 0.0):
-        """admm_solve until both residuals <= tol or max_iter."""
-        for _ in range(max_iter):
-            p, d = self.step()
-            if p <= tol_primal and d <= tol_dual:
-                break
+    def run(self, max_iter: int, tol_primal: float = 0.0, tol_dual: float = 0.0, check_every: int = 16):
+        """admm_solve until both residuals <= tol or
+        max_iter, without a host round trip per iteration (tb_admm_run: one
+        CUDA graph per iteration, device stop flag, host poll every
+        `check_every` iterations).  Single shard only."""
+        if max_iter <= 0:
+            return self.history
+        hist = np.zeros((max_iter, 2))
+        it = C.c_int32()
+        rc = self.lib.tb_admm_run(self._h, max_iter, tol_primal, tol_dual, check_every, hist.ctypes.data, C.byref(it))
+        self.history.extend((float(p), float(d)) for p, d in hist[:it.value])
+        self._check(rc)
         return self.history
+
+    def stage_times(self) -> Tuple[float, float]:
+        """Device seconds of the latest iteration's (components, consensus)
+        stages -- the per-partition batch time of SPEC.md:408."""
+        out = np.zeros(2)
+        self._check(self.lib.tb_admm_get(self._h, STAGE_TIMES, out.ctypes.data))
+        return float(out[0]), float(out[1])
+
+    def branch_errors(self) -> Tuple[int, int]:
+        """(first failed branch since the last call or -1, its status)."""
+        i, st = C.c_int64(), C.c_int32()
+        self._check(self.lib.tb_admm_branch_errors(self._h, C.byref(i), C.byref(st)))
+        return i.value, st.value
 
     # phases for the multi-process path
     def solve_components(self, stream: int = 0):
@@ -193,8 +222,9 @@ class AdmmSolver:
         self._check(self.lib.tb_admm_branch_solution(self._h, C.byref(x), C.byref(lo), C.byref(hi)))
         return x.value, lo.value, hi.value
 
-    def update_consensus(self, stream: int = 0, res2_dev_ptr: int = 0):
-        self._check(self.lib.tb_admm_update_consensus(self._h, C.c_void_p(stream or 0), C.c_void_p(res2_dev_ptr)))
+    def update_consensus(self, stream: int = 0, res3_dev_ptr: int = 0):
+        """res3_dev_ptr: 3 device doubles (primal, dual, first failed branch or -1)."""
+        self._check(self.lib.tb_admm_update_consensus(self._h, C.c_void_p(stream or 0), C.c_void_p(res3_dev_ptr)))
 
     def get(self, what: int) -> np.ndarray:
         g = self.grid
@@ -208,6 +238,8 @@ class AdmmSolver:
             out = np.zeros((g.n_branch, 36))
         elif what == BRANCH_STATUS:
             out = np.zeros(g.n_branch, np.int32)
+        elif what == STAGE_TIMES:
+            out = np.zeros(2)
         elif what in (BUS_WT, BUS_TT):
             out = np.zeros(g.n_bus)
         else:
@@ -216,10 +248,25 @@ class AdmmSolver:
         return out
 
 
+def _admm_error(rc: int, msg: str) -> Exception:
+    """The reference's exception type for a failed branch solve (batch.hpp:75-76
+    rethrows it out of solve_batch, and admm_solve propagates it)."""
+    from .tron import EvaluationError, SingularFactorError
+
+    if rc == TB_E_PROBLEM:
+        if "EvaluationError" in msg:
+            return EvaluationError(msg)
+        if "SingularFactorError" in msg:
+            return SingularFactorError(msg)
+        return ValueError(msg)
+    return SolverError(msg)
+
+
 class ShardedAdmm:
     """One process per GPU under torch.distributed (NCCL): the C5 path."""
 
-    def __init__(self, grid: Grid, rank: int, world: int, device: int, options: AdmmOptions = None):
+    def __init__(self, grid: Grid, rank: int, world: int, device: int, options: AdmmOptions = None,
+                 record_times: bool = False):
         import torch
 
         self.torch = torch
@@ -229,22 +276,56 @@ class ShardedAdmm:
         dim = (options or AdmmOptions()).branch_dim
         # the branch-solution buffer the all-gather writes into (caller-owned)
         self.x = torch.zeros((chunk * world, dim), dtype=torch.float64, device=self.dev)
-        self.res = torch.zeros(2, dtype=torch.float64, device=self.dev)
+        self.res = torch.zeros(3, dtype=torch.float64, device=self.dev)
         self.solver = AdmmSolver(grid, options, device, rank, world, x_buffer_ptr=self.x.data_ptr())
         self.history: List[Tuple[float, float]] = []
+        # per-iteration device time of this shard's branch stage (generators +
+        # branch TRON), read back lazily: partition_times() all-gathers them
+        self.record_times = record_times
+        self._ev: List[tuple] = []
 
     def step(self) -> Tuple[float, float]:
         import torch.distributed as dist
 
-        st = self.torch.cuda.current_stream(self.dev).cuda_stream
+        cs = self.torch.cuda.current_stream(self.dev)
+        st = cs.cuda_stream
         st = st if st != 0 else 1  # cudaStreamLegacy
+        if self.record_times:
+            e0, e1 = self.torch.cuda.Event(enable_timing=True), self.torch.cuda.Event(enable_timing=True)
+            e0.record(cs)
         self.solver.solve_components(st)
+        if self.record_times:
+            e1.record(cs)
+            self._ev.append((e0, e1))
         if self.world > 1:  # consensus exchange: in-place all-gather of the branch solutions
             mine = self.x[self.rank * self.chunk:(self.rank + 1) * self.chunk]
             dist.all_gather_into_tensor(self.x, mine)
         self.solver.update_consensus(st, self.res.data_ptr())
         if self.world > 1:
             dist.all_reduce(self.res, op=dist.ReduceOp.MAX)
-        p, d = self.res.tolist()
+        p, d, bad = self.res.tolist()
         self.history.append((p, d))
+        if bad >= 0:  # SPEC.md:410: a failed branch solve propagates (from every rank)
+            b = int(bad)
+            lo, hi = self.rank * self.chunk, (self.rank + 1) * self.chunk
+            st_ = int(self.solver.get(BRANCH_STATUS)[b]) if lo <= b < hi else -1
+            raise SolverError(f"ADMM branch stage: branch {b} failed with status {st_}")
         return p, d
+
+    def partition_times(self) -> List[List[float]]:
+        """[iteration][rank] seconds of the branch stage of every recorded
+        iteration (SPEC.md:408 per-partition batch times; feed imbalance())."""
+        import torch.distributed as dist
+
+        self.torch.cuda.synchronize(self.dev)
+        mine = self.torch.tensor([1e-3 * a.elapsed_time(b) for a, b in self._ev], dtype=torch_f64(self.torch),
+                                 device=self.dev)
+        if self.world == 1:
+            return [[t] for t in mine.tolist()]
+        allt = [self.torch.empty_like(mine) for _ in range(self.world)]
+        dist.all_gather(allt, mine)
+        return [list(r) for r in zip(*[a.tolist() for a in allt])]
+
+
+def torch_f64(torch):
+    return torch.float64

@@ -29,9 +29,70 @@
 
 namespace {
 
-__global__ void admm_gen_kernel(tb_admm_view v) {
+// `stop` (may be null): set once tb_admm_run's iterations have converged; the
+// stage kernels of later iterations return at once
+__device__ __forceinline__ bool stopped(const int* stop) { return stop && *stop; }
+
+__global__ void admm_gen_kernel(tb_admm_view v, const int* stop) {
+    if (stopped(stop)) return;
     const int g = blockIdx.x * blockDim.x + threadIdx.x;
     if (g < v.n_gen) tb_admm_gen_update(&v, g);
+}
+
+// Generator and branch stages in ONE launch (they run
+// concurrently): blocks [0, gen_blocks) update the generators, the others run
+// one branch TRON solve per thread (tron_thread.cuh; in place: each thread
+// reads its x0 before it writes x*).  The stages touch disjoint state.
+constexpr int kThreadBlock = 64;
+__global__ void __launch_bounds__(kThreadBlock)
+    admm_gen_branch_kernel(const __grid_constant__ tbdev::KernelArgs k, tb_admm_view v, int gen_blocks) {
+    if (stopped(k.skip)) return;
+    if ((int)blockIdx.x < gen_blocks) {
+        const int g = blockIdx.x * kThreadBlock + threadIdx.x;
+        if (g < v.n_gen) tb_admm_gen_update(&v, g);
+        return;
+    }
+    const long long pid = (long long)(blockIdx.x - gen_blocks) * kThreadBlock + threadIdx.x;
+    if (pid < k.count) tbdev::tron_solve_thread<4, TB_FAMILY_BRANCH>(k, pid);
+}
+
+// first branch of [0, n) whose solve ended where the reference throws
+// (status >= TB_STATUS_EVALUATION_ERROR), as a global branch index, into the
+// sticky slot *first (atomicMin; ~0 = none)
+__global__ void admm_status_scan_kernel(const int32_t* status, long long n, long long base,
+                                        unsigned long long* first, const int* stop) {
+    if (stopped(stop)) return;
+    const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    if (i < n && status[i] >= TB_STATUS_EVALUATION_ERROR) atomicMin(first, (unsigned long long)(base + i));
+}
+
+// tb_admm_update_consensus' export: residuals and the first failed branch of
+// the shard (-1 none) as three doubles (the caller max-allreduces them across
+// shards), and the failure record cleared for the next iteration
+__global__ void admm_export_kernel(unsigned long long* res, double* out) {
+    out[0] = __longlong_as_double((long long)res[0]);
+    out[1] = __longlong_as_double((long long)res[1]);
+    out[2] = res[2] == ~0ull ? -1.0 : (double)res[2];
+    res[2] = ~0ull;
+}
+
+// tb_admm_run: after the bus pass of one iteration, append the residuals to
+// the device history, stop once both tolerances hold (or a branch failed),
+// and clear the residual slots for the next iteration
+__global__ void admm_record_kernel(unsigned long long* res, double* hist, int* it, int cap, const double* tol,
+                                   int* stop) {
+    if (*stop) return;
+    const double p = __longlong_as_double((long long)res[0]), d = __longlong_as_double((long long)res[1]);
+    const int k = *it;
+    if (k < cap) {
+        hist[2 * k] = p;
+        hist[2 * k + 1] = d;
+    }
+    *it = k + 1;
+    if (res[2] != ~0ull) *stop = 2;
+    else if (p <= tol[0] && d <= tol[1]) *stop = 1;
+    res[0] = 0ull;
+    res[1] = 0ull;
 }
 
 // residuals are non-negative doubles: unsigned max on the bit patterns
@@ -49,7 +110,8 @@ __device__ __forceinline__ void atomic_max_nonneg(unsigned long long* a, double 
 // (one thread walked a hub bus's ends with dependent loads and divisions).
 constexpr int kBusWarps = 4;  // buses per block
 __global__ void __launch_bounds__(32 * kBusWarps)
-    admm_bus_warp_kernel(tb_admm_view v, int res_lo, int res_hi, unsigned long long* res) {
+    admm_bus_warp_kernel(tb_admm_view v, int res_lo, int res_hi, unsigned long long* res, const int* stop) {
+    if (stopped(stop)) return;
     __shared__ double stage[kBusWarps][8][32];
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     const int b = blockIdx.x * kBusWarps + w;
@@ -208,7 +270,7 @@ __global__ void __launch_bounds__(32, tbdev::WarpMinBlocks<6>::value)
                              int* round_max) {
     extern __shared__ double smem[];
     const long long pid = blockIdx.x;
-    if (pid >= a.count) return;
+    if (pid >= a.count || stopped(a.skip)) return;
     const int lane = threadIdx.x & 31;
     double* prm = prm_shard + pid * TB_BR_NPARAMS;
     if (lane == 0) {
@@ -231,7 +293,8 @@ __global__ void __launch_bounds__(32, tbdev::WarpMinBlocks<6>::value)
     if (lane == 0) atomicMax(round_max, rounds);
 }
 
-__global__ void admm_round_accum_kernel(int* round_max, long long* total) {
+__global__ void admm_round_accum_kernel(int* round_max, long long* total, const int* stop) {
+    if (stopped(stop)) return;
     *total += *round_max;
     *round_max = 0;
 }
@@ -273,8 +336,22 @@ struct tb_admm {
     double* x = nullptr;        // [n_rows][4] branch solutions (owned or caller's)
     double *lower = nullptr, *upper = nullptr;
     int32_t* status = nullptr;
+    // res[0..1]: residual maxima (IEEE bits of non-negative doubles), res[2]:
+    // first failed branch of the shard (sticky until the next step / run; ~0 none)
     unsigned long long* res = nullptr;
     double* cost = nullptr;
+    // tb_admm_run: stop flag, iteration counter, residual history, tolerances,
+    // and the captured CUDA graph of one iteration
+    int* stop = nullptr;
+    int* it_dev = nullptr;
+    double* hist = nullptr;
+    int hist_cap = 0;
+    double* tol = nullptr;
+    cudaGraphExec_t graph = nullptr;
+    // stage timing of the latest iteration: [0] components start, [1] branch
+    // stage done, [2] consensus done
+    cudaEvent_t ev[3] = {nullptr, nullptr, nullptr};
+    int branch_form = TB_FORM_AUTO;
     int64_t br_lo = 0, br_hi = 0;
     int bus_lo = 0, bus_hi = 0;
     tb_tron_config tron{};
@@ -356,10 +433,15 @@ int tb_admm_create(const tb_admm_grid* gr, const tb_admm_options* opt, int32_t d
             return fail(TB_E_INVALID_ARGUMENT, "tb_admm_create: bus " + std::to_string(b) + " has no branch");
         }
 
+    if (opt->branch_form != TB_FORM_AUTO && opt->branch_form != TB_FORM_WARP) {
+        tb_admm_host_free(&hs);
+        return fail(TB_E_INVALID_ARGUMENT, "tb_admm_create: branch_form must be TB_FORM_AUTO or TB_FORM_WARP");
+    }
     tb_admm* a = new tb_admm;
     a->device = device;
     a->tron = opt->tron;
     a->opt = *opt;
+    a->branch_form = opt->branch_form;
     const int D = hs.dim;
     a->dim = D;
     int prev = 0;
@@ -430,8 +512,16 @@ int tb_admm_create(const tb_admm_grid* gr, const tb_admm_options* opt, int32_t d
         a->upper = dalloc<double>(a, (size_t)nl * D, &err);
         if (err == cudaSuccess) err = upload<double>(a->upper, hs.br_upper, (size_t)nl * D);
         a->status = dalloc<int32_t>(a, (size_t)nl, &err);
-        a->res = dalloc<unsigned long long>(a, 2, &err);
+        a->res = dalloc<unsigned long long>(a, 3, &err);
         a->cost = dalloc<double>(a, 1, &err);
+        a->stop = dalloc<int>(a, 2, &err);
+        if (err == cudaSuccess) a->it_dev = a->stop + 1;
+        a->tol = dalloc<double>(a, 2, &err);
+        if (err == cudaSuccess) err = cudaMemset(a->res, 0, 2 * sizeof(unsigned long long));
+        if (err == cudaSuccess) err = cudaMemset(a->res + 2, 0xff, sizeof(unsigned long long));
+        if (err == cudaSuccess) err = cudaMemset(a->stop, 0, 2 * sizeof(int));
+        if (err == cudaSuccess) err = cudaMemset(a->status, 0, sizeof(int32_t) * (size_t)nl);
+        for (int k = 0; k < 3 && err == cudaSuccess; ++k) err = cudaEventCreate(&a->ev[k]);
     }
     if (err == cudaSuccess && D == 6) {  // AL state
         a->eta = dalloc<double>(a, (size_t)nl, &err);
@@ -462,6 +552,9 @@ int tb_admm_destroy(tb_admm* a) {
     cudaGetDevice(&prev);
     cudaSetDevice(a->device);
     if (a->stream) cudaStreamSynchronize(a->stream);
+    if (a->graph) cudaGraphExecDestroy(a->graph);
+    for (auto& e : a->ev)
+        if (e) cudaEventDestroy(e);
     for (void* p : a->allocs) cudaFree(p);
     if (a->stream) cudaStreamDestroy(a->stream);
     if (a->ctx) tb_context_destroy(a->ctx);
@@ -470,83 +563,122 @@ int tb_admm_destroy(tb_admm* a) {
     return TB_OK;
 }
 
-// generator update (all generators) + branch TRON on this shard, enqueued on
-// `stream` (NULL: the ADMM's own stream); returns without synchronising.
-// d = 4 branch stage form: thread per branch unless TB_ADMM_WARP=1
-static bool thread_form() {
-    static const bool t = [] {
-        const char* e = getenv("TB_ADMM_WARP");
-        return !(e && e[0] == '1');
-    }();
-    return t;
+namespace {
+
+bool capturing(cudaStream_t st) {
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    return cudaStreamIsCapturing(st, &cs) == cudaSuccess && cs != cudaStreamCaptureStatusNone;
 }
 
-int tb_admm_solve_components(tb_admm* a, void* stream) {
-    if (!a) return fail(TB_E_INVALID_ARGUMENT, "null admm");
-    DeviceGuard guard(a->device);
-    cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : a->stream;
-    a->last = st;
-    if (a->v.n_gen > 0) {
-        admm_gen_kernel<<<(a->v.n_gen + 127) / 128, 128, 0, st>>>(a->v);
-        tbdev::note_launches(1);
-    }
+// generator + branch stage of this shard on `st` (`stop`: tb_admm_run's flag
+// or null), then the status scan into res[2]
+int enqueue_components(tb_admm* a, cudaStream_t st, const int* stop) {
+    const bool timed = !capturing(st);
+    if (timed) cudaEventRecord(a->ev[0], st);
     const int64_t cnt = a->br_hi - a->br_lo;
+    const int gen_blocks = (a->v.n_gen + kThreadBlock - 1) / kThreadBlock;
+    tbdev::KernelArgs k{};
+    k.nparams = TB_BR_NPARAMS;
+    k.count = cnt;
+    k.stride = TB_BR_NPARAMS;
+    k.cfg = a->tron;
+    k.fast_forward = 1;
+    k.extrap = 1.0 / a->tron.interp_factor;
+    k.prm = a->v.br_params + a->br_lo * TB_BR_NPARAMS;
+    k.status = a->status + a->br_lo;
+    k.skip = stop;
+    k.form = a->branch_form;
     if (cnt > 0 && a->dim == 6) {
         // the whole augmented-Lagrangian loop of every branch in one launch
-        tbdev::KernelArgs k{};
+        if (a->v.n_gen > 0) {
+            admm_gen_kernel<<<(a->v.n_gen + 127) / 128, 128, 0, st>>>(a->v, stop);
+            tbdev::note_launches(1);
+        }
         k.n = 6;
-        k.nparams = TB_BR_NPARAMS;
-        k.count = cnt;
-        k.stride = TB_BR_NPARAMS;
         k.x0 = a->x + a->br_lo * 6;
         k.lo = a->lower + a->br_lo * 6;
         k.up = a->upper + a->br_lo * 6;
-        k.prm = a->v.br_params + a->br_lo * TB_BR_NPARAMS;
-        k.cfg = a->tron;
-        k.fast_forward = 1;
-        k.extrap = 1.0 / a->tron.interp_factor;
         k.x_star = a->x + a->br_lo * 6;  // in place
-        k.status = a->status + a->br_lo;
         // (a thread-per-branch form of this loop measured 184 vs 283 iter/s on C4: the AL
         // rounds make the stage throughput-bound, where the warp form wins)
         const size_t smem = sizeof(double) * (size_t)(tbdev::SmemLayout<6>::fixed() + TB_BR_NPARAMS);
         admm_auglag_fused_kernel<<<(unsigned)cnt, 32, smem, st>>>(
             k, a->v.br_params + a->br_lo * TB_BR_NPARAMS, a->eta + a->br_lo, a->opt.auglag_xi0, a->opt.auglag_eta0,
             a->opt.auglag_feas_tol, a->opt.auglag_xi_max, a->opt.auglag_max_iter, a->round_max);
-        admm_round_accum_kernel<<<1, 1, 0, st>>>(a->round_max, a->rounds_total);
+        admm_round_accum_kernel<<<1, 1, 0, st>>>(a->round_max, a->rounds_total, stop);
         tbdev::note_launches(2);
-    } else if (cnt > 0 && thread_form()) {
-        // one thread per branch (tron_thread.cuh): the stage waits for its
-        // slowest branch, whose latency this form cuts
-        tbdev::KernelArgs k{};
+    } else if (a->branch_form == TB_FORM_AUTO) {
+        // generators and one thread per branch (tron_thread.cuh) in one
+        // launch: the stage waits for its slowest branch, whose latency this
+        // form cuts
         k.n = 4;
-        k.nparams = TB_BR_NPARAMS;
-        k.count = cnt;
-        k.stride = TB_BR_NPARAMS;
         k.x0 = a->x + a->br_lo * 4;
         k.lo = a->lower + a->br_lo * 4;
         k.up = a->upper + a->br_lo * 4;
-        k.prm = a->v.br_params + a->br_lo * TB_BR_NPARAMS;
-        k.cfg = a->tron;
-        k.fast_forward = 1;
-        k.extrap = 1.0 / a->tron.interp_factor;
         k.x_star = a->x + a->br_lo * 4;  // in place: each thread reads its x0 first
-        k.status = a->status + a->br_lo;
-        tbdev::tron_thread_kernel<4><<<(unsigned)((cnt + 63) / 64), 64, 0, st>>>(k);
-        tbdev::note_launches(1);
-    } else if (cnt > 0) {
-        tb_problem_batch b{TB_FAMILY_BRANCH, 4, cnt, a->x + a->br_lo * 4, a->lower + a->br_lo * 4,
-                           a->upper + a->br_lo * 4, a->v.br_params + a->br_lo * TB_BR_NPARAMS, TB_BR_NPARAMS,
-                           TB_MEM_DEVICE};
-        tb_batch_result r{};
-        r.x_star = a->x + a->br_lo * 4;  // in place: each warp reads its x0 before writing x*
-        r.status = a->status + a->br_lo;
-        r.memspace = TB_MEM_DEVICE;
-        const int rc = tb_solve_batch_async(a->ctx, &b, &a->tron, &r, st);
-        if (rc != TB_OK) return fail(rc, tb_last_error());
+        const long long blocks = gen_blocks + (cnt + kThreadBlock - 1) / kThreadBlock;
+        if (blocks > 0) {
+            admm_gen_branch_kernel<<<(unsigned)blocks, kThreadBlock, 0, st>>>(k, a->v, gen_blocks);
+            tbdev::note_launches(1);
+        }
+    } else {
+        // warp per branch (KernelForm.WARP) through the library's launcher
+        if (a->v.n_gen > 0) {
+            admm_gen_kernel<<<(a->v.n_gen + 127) / 128, 128, 0, st>>>(a->v, stop);
+            tbdev::note_launches(1);
+        }
+        if (cnt > 0) {
+            k.n = 4;
+            k.x0 = a->x + a->br_lo * 4;
+            k.lo = a->lower + a->br_lo * 4;
+            k.up = a->upper + a->br_lo * 4;
+            k.x_star = a->x + a->br_lo * 4;  // in place: each warp reads its x0 before writing x*
+            k.route_count = cnt;
+            const cudaError_t e = tbdev::launch_tron(TB_FAMILY_BRANCH, k, st);
+            if (e != cudaSuccess) return fail(TB_E_CUDA, cudaGetErrorString(e));
+        }
     }
+    if (cnt > 0) {
+        admm_status_scan_kernel<<<(unsigned)((cnt + 255) / 256), 256, 0, st>>>(a->status + a->br_lo, cnt, a->br_lo,
+                                                                             a->res + 2, stop);
+        tbdev::note_launches(1);
+    }
+    if (timed) cudaEventRecord(a->ev[1], st);
     const cudaError_t e = cudaGetLastError();
     return e == cudaSuccess ? TB_OK : fail(TB_E_CUDA, cudaGetErrorString(e));
+}
+
+int enqueue_consensus(tb_admm* a, cudaStream_t st, const int* stop) {
+    admm_bus_warp_kernel<<<(a->v.n_bus + kBusWarps - 1) / kBusWarps, 32 * kBusWarps, 0, st>>>(a->v, a->bus_lo,
+                                                                                             a->bus_hi, a->res, stop);
+    tbdev::note_launches(1);
+    if (!capturing(st)) cudaEventRecord(a->ev[2], st);
+    const cudaError_t e = cudaGetLastError();
+    return e == cudaSuccess ? TB_OK : fail(TB_E_CUDA, cudaGetErrorString(e));
+}
+
+std::string branch_error_message(tb_admm* a, unsigned long long idx) {
+    int32_t st = 0;
+    cudaMemcpy(&st, a->status + idx, sizeof st, cudaMemcpyDeviceToHost);
+    const char* what = st == TB_STATUS_EVALUATION_ERROR ? "EvaluationError"
+                       : st == TB_STATUS_ZERO_DIRECTION ? "invalid_argument (trqsol: zero direction)"
+                       : st == TB_STATUS_SINGULAR_FACTOR ? "SingularFactorError"
+                                                         : "invalid_argument (bounds)";
+    return "ADMM branch stage: branch " + std::to_string(idx) + " failed with status " + std::to_string(st) + " (" +
+           what + ")";
+}
+
+}  // namespace
+
+// generator update (all generators) + branch TRON on this shard, enqueued on
+// `stream` (NULL: the ADMM's own stream); returns without synchronising.
+// Branch failures are recorded on the device (tb_admm_branch_errors).
+int tb_admm_solve_components(tb_admm* a, void* stream) {
+    if (!a) return fail(TB_E_INVALID_ARGUMENT, "null admm");
+    DeviceGuard guard(a->device);
+    cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : a->stream;
+    a->last = st;
+    return enqueue_components(a, st, nullptr);
 }
 
 // device branch-solution buffer [rows][4]; this shard owns rows [lo, hi);
@@ -559,39 +691,143 @@ int tb_admm_branch_solution(tb_admm* a, double** x_dev, int64_t* lo, int64_t* hi
     return TB_OK;
 }
 
-// bus consensus + multipliers over every bus (needs the complete x), residual
-// maxima over this shard's buses written to res2_dev[0..1] (device doubles) if
-// non-NULL; enqueued on `stream`.
-int tb_admm_update_consensus(tb_admm* a, void* stream, double* res2_dev) {
+// bus consensus + multipliers over every bus (needs the complete x); if
+// res3_dev is non-NULL: residual maxima over this shard's buses in
+// res3_dev[0..1] and the shard's first failed branch (-1 none) in res3_dev[2]
+// (device doubles); enqueued on `stream`.
+int tb_admm_update_consensus(tb_admm* a, void* stream, double* res3_dev) {
     if (!a) return fail(TB_E_INVALID_ARGUMENT, "null admm");
     DeviceGuard guard(a->device);
     cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : a->stream;
     a->last = st;
     cudaMemsetAsync(a->res, 0, 2 * sizeof(unsigned long long), st);
-    admm_bus_warp_kernel<<<(a->v.n_bus + kBusWarps - 1) / kBusWarps, 32 * kBusWarps, 0, st>>>(a->v, a->bus_lo,
-                                                                                             a->bus_hi, a->res);
-    tbdev::note_launches(1);
-    if (res2_dev) cudaMemcpyAsync(res2_dev, a->res, 2 * sizeof(double), cudaMemcpyDeviceToDevice, st);
+    int rc = enqueue_consensus(a, st, nullptr);
+    if (rc) return rc;
+    if (res3_dev) {
+        admm_export_kernel<<<1, 1, 0, st>>>(a->res, res3_dev);
+        tbdev::note_launches(1);
+    }
     ++a->iterations;
     const cudaError_t e = cudaGetLastError();
     return e == cudaSuccess ? TB_OK : fail(TB_E_CUDA, cudaGetErrorString(e));
 }
 
+// first failed branch of this shard since the last call (blocking; -1: none),
+// and its status; clears the record
+int tb_admm_branch_errors(tb_admm* a, int64_t* first_bad, int32_t* status) {
+    if (!a || !first_bad) return fail(TB_E_INVALID_ARGUMENT, "null argument");
+    DeviceGuard guard(a->device);
+    if (a->last && a->last != a->stream) cudaStreamSynchronize(a->last);
+    unsigned long long idx = ~0ull;
+    cudaError_t e = cudaMemcpy(&idx, a->res + 2, sizeof idx, cudaMemcpyDeviceToHost);
+    if (e == cudaSuccess) e = cudaMemset(a->res + 2, 0xff, sizeof idx);
+    if (e != cudaSuccess) return fail(TB_E_CUDA, cudaGetErrorString(e));
+    *first_bad = idx == ~0ull ? -1 : (int64_t)idx;
+    if (status) {
+        *status = 0;
+        if (idx != ~0ull) cudaMemcpy(status, a->status + idx, sizeof *status, cudaMemcpyDeviceToHost);
+    }
+    return TB_OK;
+}
+
 // one full iteration in a single process (no exchange needed), blocking;
-// primal / dual residuals to host
+// primal / dual residuals to host.  TB_E_PROBLEM if a branch solve ended
+// where the reference would throw (the state is advanced regardless).
 int tb_admm_step(tb_admm* a, double* primal, double* dual) {
     if (!a) return fail(TB_E_INVALID_ARGUMENT, "null admm");
     DeviceGuard guard(a->device);
-    int rc = tb_admm_solve_components(a, nullptr);
+    a->last = a->stream;
+    cudaMemsetAsync(a->res + 2, 0xff, sizeof(unsigned long long), a->stream);
+    int rc = enqueue_components(a, a->stream, nullptr);
     if (rc) return rc;
     rc = tb_admm_update_consensus(a, nullptr, nullptr);
     if (rc) return rc;
-    double r[2];
+    unsigned long long r[3];
     cudaError_t e = cudaMemcpyAsync(r, a->res, sizeof r, cudaMemcpyDeviceToHost, a->stream);
     if (e == cudaSuccess) e = cudaStreamSynchronize(a->stream);
     if (e != cudaSuccess) return fail(TB_E_CUDA, cudaGetErrorString(e));
-    if (primal) *primal = r[0];
-    if (dual) *dual = r[1];
+    if (primal) std::memcpy(primal, &r[0], sizeof(double));
+    if (dual) std::memcpy(dual, &r[1], sizeof(double));
+    if (r[2] != ~0ull) return fail(TB_E_PROBLEM, branch_error_message(a, r[2]));
+    return TB_OK;
+}
+
+// admm_solve on one process without a host round trip per
+// iteration: one iteration (stages + residual record) is captured once as a
+// CUDA graph and replayed; the record kernel raises a device stop flag at the
+// first iteration whose residuals are both <= tol (or whose branch stage
+// failed), and every stage kernel of the iterations enqueued after it returns
+// at once, so the state equals stopping exactly there.  The host checks the
+// flag every `check_every` iterations.  hist_out: [max_iter][2] residuals
+// (may be NULL); *iters_out: iterations run.
+int tb_admm_run(tb_admm* a, int32_t max_iter, double tol_primal, double tol_dual, int32_t check_every,
+                double* hist_out, int32_t* iters_out) {
+    if (!a || !iters_out) return fail(TB_E_INVALID_ARGUMENT, "null argument");
+    if (max_iter < 0 || check_every < 1) return fail(TB_E_INVALID_ARGUMENT, "tb_admm_run: bad max_iter / check_every");
+    if (a->br_lo != 0 || a->br_hi != a->v.n_branch)
+        return fail(TB_E_INVALID_ARGUMENT, "tb_admm_run: single-shard ADMM only (sharded runs exchange per iteration)");
+    DeviceGuard guard(a->device);
+    cudaStream_t st = a->stream;
+    a->last = st;
+    cudaError_t e = cudaSuccess;
+    if (max_iter > a->hist_cap) {
+        if (a->graph) {  // the graph holds the old history pointer
+            cudaGraphExecDestroy(a->graph);
+            a->graph = nullptr;
+        }
+        a->hist = dalloc<double>(a, (size_t)2 * max_iter, &e);
+        if (e != cudaSuccess) return fail(TB_E_CUDA, cudaGetErrorString(e));
+        a->hist_cap = max_iter;
+    }
+    const double tol[2] = {tol_primal, tol_dual};
+    e = cudaMemcpyAsync(a->tol, tol, sizeof tol, cudaMemcpyHostToDevice, st);
+    if (e == cudaSuccess) e = cudaMemsetAsync(a->stop, 0, 2 * sizeof(int), st);
+    if (e == cudaSuccess) e = cudaMemsetAsync(a->res, 0, 2 * sizeof(unsigned long long), st);
+    if (e == cudaSuccess) e = cudaMemsetAsync(a->res + 2, 0xff, sizeof(unsigned long long), st);
+    if (e != cudaSuccess) return fail(TB_E_CUDA, cudaGetErrorString(e));
+    if (!a->graph) {
+        cudaGraph_t g = nullptr;
+        e = cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal);
+        if (e != cudaSuccess) return fail(TB_E_CUDA, cudaGetErrorString(e));
+        int rc = enqueue_components(a, st, a->stop);
+        if (rc == TB_OK) rc = enqueue_consensus(a, st, a->stop);
+        if (rc == TB_OK) {
+            admm_record_kernel<<<1, 1, 0, st>>>(a->res, a->hist, a->it_dev, a->hist_cap, a->tol, a->stop);
+            tbdev::note_launches(1);
+        }
+        e = cudaStreamEndCapture(st, &g);
+        if (rc) {
+            if (g) cudaGraphDestroy(g);
+            return rc;
+        }
+        if (e == cudaSuccess) e = cudaGraphInstantiate(&a->graph, g, 0);
+        if (g) cudaGraphDestroy(g);
+        if (e != cudaSuccess) return fail(TB_E_CUDA, cudaGetErrorString(e));
+    }
+    int done = 0, it = 0, stop = 0;
+    while (done < max_iter) {
+        const int k = std::min<int>(check_every, max_iter - done);
+        for (int i = 0; i < k && e == cudaSuccess; ++i) e = cudaGraphLaunch(a->graph, st);
+        done += k;
+        int flags[2] = {0, 0};
+        if (e == cudaSuccess) e = cudaMemcpyAsync(flags, a->stop, sizeof flags, cudaMemcpyDeviceToHost, st);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+        if (e != cudaSuccess) return fail(TB_E_CUDA, cudaGetErrorString(e));
+        stop = flags[0];
+        it = flags[1];
+        if (stop) break;
+    }
+    a->iterations += it;
+    *iters_out = it;
+    if (hist_out && it > 0) {
+        e = cudaMemcpy(hist_out, a->hist, sizeof(double) * 2 * (size_t)it, cudaMemcpyDeviceToHost);
+        if (e != cudaSuccess) return fail(TB_E_CUDA, cudaGetErrorString(e));
+    }
+    if (stop == 2) {
+        unsigned long long idx = ~0ull;
+        cudaMemcpy(&idx, a->res + 2, sizeof idx, cudaMemcpyDeviceToHost);
+        return fail(TB_E_PROBLEM, branch_error_message(a, idx));
+    }
     return TB_OK;
 }
 
@@ -636,6 +872,16 @@ int tb_admm_get(tb_admm* a, int32_t what, void* host_out) {
         }
         case TB_ADMM_BRANCH_PARAMS: src = v.br_params; bytes = sizeof(double) * TB_BR_NPARAMS * (size_t)v.n_branch; break;
         case TB_ADMM_BRANCH_STATUS: src = a->status; bytes = sizeof(int32_t) * (size_t)v.n_branch; break;
+        case TB_ADMM_STAGE_TIMES: {  // seconds: [components (generators + branch TRON), consensus pass]
+            float ms[2] = {0.f, 0.f};
+            cudaError_t e = cudaEventSynchronize(a->ev[2]);
+            if (e == cudaSuccess) e = cudaEventElapsedTime(&ms[0], a->ev[0], a->ev[1]);
+            if (e == cudaSuccess) e = cudaEventElapsedTime(&ms[1], a->ev[1], a->ev[2]);
+            if (e != cudaSuccess) return fail(TB_E_CUDA, cudaGetErrorString(e));
+            const double t[2] = {1e-3 * ms[0], 1e-3 * ms[1]};
+            std::memcpy(host_out, t, sizeof t);
+            return TB_OK;
+        }
         case TB_ADMM_COST: {
             admm_cost_kernel<<<1, 1, 0, a->stream>>>(a->v, a->cost);
             src = a->cost;

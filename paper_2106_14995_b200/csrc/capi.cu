@@ -364,6 +364,7 @@ tbdev::KernelArgs make_args(const tb_problem_batch* b, int64_t np, const tb_tron
     a.route_count = cnt;
     a.next = nullptr;
     a.form = form;
+    a.skip = nullptr;
     return a;
 }
 

@@ -124,6 +124,9 @@ struct KernelArgs {
     // the launch stream before the launch
     unsigned long long* next;
     int form;  // TB_FORM_* requested by the context (routing only)
+    // device flag: when non-null and set, the launch does nothing (ADMM
+    // iterations enqueued past convergence, tb_admm_run)
+    const int* skip;
 };
 
 // shared memory per warp (doubles; every region starts at an even offset)
@@ -1164,7 +1167,7 @@ template <int FAM, int D, bool COUNT>
 __global__ void __launch_bounds__(32, WarpMinBlocks<D>::value) tron_solve_kernel(const __grid_constant__ KernelArgs a) {
     extern __shared__ double smem[];
     const long long pid = blockIdx.x;
-    if (pid >= a.count) return;
+    if (pid >= a.count || (a.skip && *a.skip)) return;
     tron_solve_one<FAM, D, COUNT>(a, pid, smem);
 }
 

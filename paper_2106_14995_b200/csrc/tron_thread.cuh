@@ -670,7 +670,7 @@ __device__ __forceinline__ void tron_solve_thread(const KernelArgs& a, const lon
 template <int D, int FAM = TB_FAMILY_BRANCH>
 __global__ void __launch_bounds__(64) tron_thread_kernel(const __grid_constant__ KernelArgs a) {
     const long long pid = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-    if (pid >= a.count) return;
+    if (pid >= a.count || (a.skip && *a.skip)) return;
     tron_solve_thread<D, FAM>(a, pid);
 }
 

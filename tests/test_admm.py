@@ -318,28 +318,14 @@ def test_get_after_stages_on_caller_stream_sees_their_results():
 
 @pytest.mark.gpu
 def test_thread_and_warp_branch_stage_forms_agree_bitwise():
-    """The d = 4 branch stage runs one thread per branch by default
-    (csrc/tron_thread.cuh) and the warp kernel with TB_ADMM_WARP=1; both are
-    bit-identical to the oracle, hence to each other (state after 12
-    iterations, compared across two processes)."""
-    import os
-    import subprocess
-    import sys
-
-    code = (
-        "import sys, numpy as np; sys.path.insert(0, '.');"
-        "from paper_2106_14995_b200 import admm as A, synth;"
-        "g = synth.grid(800, 1100, 240, seed=9, shunt_frac=0.3); s = A.AdmmSolver(g);"
-        "h = [s.step() for _ in range(12)];"
-        "np.save(sys.argv[1], np.concatenate([np.ravel(h), s.get(A.BRANCH_X).ravel(), s.get(A.BRANCH_PARAMS).ravel(),"
-        " s.get(A.BUS_WT), s.get(A.GEN_P)]))"
-    )
-    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    out = {}
-    for form, env in (("thread", {}), ("warp", {"TB_ADMM_WARP": "1"})):
-        path = os.path.join(root, "gpurun_out" if os.path.isdir(os.path.join(root, "gpurun_out")) else ".",
-                            f"_admm_form_{form}.npy")
-        subprocess.run([sys.executable, "-c", code, path], cwd=root, env=dict(os.environ, **env), check=True)
-        out[form] = np.load(path)
-        os.remove(path)
-    assert np.array_equal(out["thread"].view(np.int64), out["warp"].view(np.int64))
+    """The d = 4 branch stage runs one thread per branch, fused with the
+    generator updates, by default (csrc/tron_thread.cuh) and the warp kernel
+    with branch_form="warp"; both are bit-identical to the oracle, hence to
+    each other (residuals every iteration and the state after 12)."""
+    g = synth.grid(800, 1100, 240, seed=9, shunt_frac=0.3)
+    t = A.AdmmSolver(g)
+    w = A.AdmmSolver(g, A.AdmmOptions(branch_form="warp"))
+    for k in range(12):
+        assert t.step() == w.step(), k
+    for what in (A.BRANCH_X, A.BRANCH_PARAMS, A.BUS_WT, A.GEN_P, A.GEN_LP):
+        assert np.array_equal(t.get(what), w.get(what)), what
