@@ -42,12 +42,24 @@ WORKLOAD = "C2: 65,536 synthetic AC-OPF branch augmented-Lagrangian subproblems 
 
 def kernel_form(d, count):
     """Which device kernel the library routes a (dim, count) ncvx batch to
-    (csrc/tron_kernels_ncvx.cu, tron_thread.cuh)."""
-    if d == 4 and count >= int(os.environ.get("TB_THREAD_MIN", 16384)) and os.environ.get("TB_THREAD") != "0":
+    under KernelForm.AUTO (csrc/tron_kernels.cuh resolve_form)."""
+    if d == 4 and count >= 16384:
         return "thread per problem"
     if d <= 16:
         return "warp per problem"
     return f"block of {32 if d <= 32 else 64 if d <= 64 else 128} threads (persistent)"
+
+def sig(x, digits=5):
+    """Round floats in a nested structure to `digits` significant digits
+    (keeps the ADMM block short enough for the driver's 1,500-char tail)."""
+    if isinstance(x, float):
+        return float(f"{x:.{digits}g}")
+    if isinstance(x, dict):
+        return {k: sig(v, digits) for k, v in x.items()}
+    if isinstance(x, (list, tuple)):
+        return [sig(v, digits) for v in x]
+    return x
+
 
 def env_int(k, d):
     try:
@@ -191,69 +203,192 @@ def run_reference_arm(args, rank, world):
     return 0
 
 
+def c5_grid():
+    from paper_2106_14995_b200 import synth
+
+    nb = int(round(70000 * 13659 / 20467))  # C4's bus / branch ratio: 46,716 buses
+    return synth.grid(nb, 70000, int(0.3 * nb))
+
+
+def replay_imbalance(grid, dev, iters=5, parts=(2, 4, 8)):
+    """SPEC.md:408 / PAPER.md:689-703 per-GPU imbalance of the C5 branch stage
+    at G = 2 / 4 / 8, measured on one GPU: after each ADMM iteration the branch
+    batch (warm starts, current multipliers) is snapshotted and every
+    partition's share is solved alone (its kernel time = what one GPU of a
+    G-GPU run spends on it).  Contiguous even partitions (batch.hpp:61-70, the
+    paper's dispatch) against a cost-aware one (LPT over the per-branch device
+    times of the PREVIOUS iteration's snapshot, PAPER.md:715 future work)."""
+    import torch
+
+    from paper_2106_14995_b200 import ProblemBatch, Solver, imbalance
+    from paper_2106_14995_b200 import admm as A
+
+    run = A.AdmmSolver(grid, device=dev.index)
+    for _ in range(3):
+        run.step()
+    solver = Solver((dev.index,))
+    n = grid.n_branch
+    t = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(dev)  # noqa: E731
+    lo = np.stack([grid.bus_vmin[grid.br_from], grid.bus_vmin[grid.br_to], np.full(n, -2 * np.pi),
+                   np.full(n, -2 * np.pi)], axis=1)
+    up = np.stack([grid.bus_vmax[grid.br_from], grid.bus_vmax[grid.br_to], np.full(n, 2 * np.pi),
+                   np.full(n, 2 * np.pi)], axis=1)
+    dlo, dup = t(lo), t(up)
+
+    def part_time(b, idx):
+        sub = ProblemBatch(b.family, 4, b.lower[idx], b.upper[idx], b.params[idx], b.x0[idx])
+        out = Solver.alloc_result(len(idx), 4, device=True)
+        solver.solve_batch(sub, out=out)  # warm-up launch of the same share
+        solver.solve_batch(sub, out=out)
+        return out.kernel_time
+
+    prev_cost = None
+    times = {("contiguous", G): [] for G in parts}
+    times.update({("cost_aware", G): [] for G in parts})
+    for _ in range(iters):
+        run.step()
+        b = ProblemBatch(3, 4, dlo, dup, t(run.get(A.BRANCH_PARAMS)), t(run.get(A.BRANCH_X)))
+        full = Solver.alloc_result(n, 4, device=True)
+        solver.solve_batch(b, out=full)
+        cost = full.per_problem_time.cpu().numpy()
+        for G in parts:
+            cut = [n * k // G for k in range(G + 1)]
+            idx = [torch.arange(cut[k], cut[k + 1], device=dev) for k in range(G)]
+            times[("contiguous", G)].append([part_time(b, i) for i in idx])
+            if prev_cost is not None:  # LPT on last iteration's per-branch times
+                order = np.argsort(-prev_cost, kind="stable")
+                load = np.zeros(G)
+                owner = np.empty(n, np.int64)
+                for j in order:
+                    k = int(np.argmin(load))
+                    owner[j] = k
+                    load[k] += prev_cost[j]
+                idx = [torch.from_numpy(np.nonzero(owner == k)[0]).to(dev) for k in range(G)]
+                times[("cost_aware", G)].append([part_time(b, i) for i in idx])
+        prev_cost = cost
+    run.close()
+    solver.close()
+    out = {}
+    for (kind, G), tt in times.items():
+        if tt:
+            st = imbalance(tt)
+            out.setdefault(kind, {})[f"G{G}"] = {"nu_max": round(st.nu_max, 1), "nu_min": round(st.nu_min, 1),
+                                                 "nu_mean": round(st.nu_mean, 1),
+                                                 "max_part_ms": round(1e3 * max(max(r) for r in tt), 3)}
+    out["method"] = ("one GPU, each partition's share of the C5 branch stage solved alone (kernel time) on "
+                     f"{iters} successive ADMM iterations; cost-aware = LPT over the previous iteration's "
+                     "per-branch device times")
+    return out
+
+
+def admm_summary(line):
+    """The ADMM numbers without their descriptions (those are in admm_detail)."""
+    if not line:
+        return line
+    out = {"metric": line["metric"], "value": line["value"], "unit": line["unit"],
+           "ms_per_iter": line["ms_per_iter"], "workload": line["config"]["workload"]}
+    for k in ("per_step", "line_limits", "cpu_baseline"):
+        if isinstance(line.get(k), dict):
+            out[k] = line[k].get("value")
+    if "imbalance" in line:
+        out["imbalance"] = {k: line["imbalance"][k] for k in ("nu_max", "nu_min", "nu_mean")}
+    if "c5" in line:
+        c5 = line["c5"]
+        out["c5"] = {"value": c5["value"], "ms_per_iter": c5["ms_per_iter"]}
+        rep = c5.get("imbalance_replay") or {}
+        out["c5"]["nu_mean_contiguous_vs_cost_aware"] = {
+            G: [rep.get("contiguous", {}).get(G, {}).get("nu_mean"), rep.get("cost_aware", {}).get(G, {}).get("nu_mean")]
+            for G in ("G2", "G4", "G8")}
+    return sig(out, 4)
+
+
 def run_admm(args, rank, world, local, dev):
-    """ADMM iterations/s: C4 (13,659 buses / 20,467 branches / 4,092 gens) on
-    one GPU; C5 (70,000 branches, ~46.7k buses) sharded over N GPUs with an
-    NCCL all-gather of the branch solutions + max-allreduce of the residuals
-    per iteration.  Each timed iteration = generator + branch TRON + exchange +
-    bus/multiplier/residual kernels + the residual read-back."""
+    """ADMM iterations/s.  N = 1: C4 (13,659 buses / 20,467 branches / 4,092
+    gens) through tb_admm_run (one CUDA graph per iteration, device stop flag,
+    no host round trip per iteration) and through the per-iteration blocking
+    step, C4 with line limits, and C5 (70,000 branches, 46,716 buses) through
+    the sharded driver at world 1 plus its replayed G = 2/4/8 imbalance.
+    N > 1: C5 sharded over N GPUs (NCCL all-gather of the branch solutions +
+    max-allreduce of the residuals per iteration), per-rank branch-stage times
+    -> imbalance."""
     import torch
     import torch.distributed as dist
 
     from paper_2106_14995_b200 import admm as A
-    from paper_2106_14995_b200 import synth
+    from paper_2106_14995_b200 import imbalance, synth
 
-    if world == 1:
-        cfg, grid = "C4", synth.grid(13659, 20467, 4092)
-    else:
-        nb = int(round(70000 * 13659 / 20467))
-        cfg, grid = "C5", synth.grid(nb, 70000, int(0.3 * nb))
-    if world > 1 and not dist.is_initialized():
-        return None
-    run = A.ShardedAdmm(grid, rank, world, local)
-    for _ in range(max(3, args.warmup)):
-        run.step()
-    stream = torch.cuda.current_stream(dev)
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    if world > 1:
-        dist.barrier()
-    torch.cuda.synchronize(dev)
-    e0.record(stream)
-    for _ in range(args.admm_iters):
-        run.step()
-    e1.record(stream)
-    torch.cuda.synchronize(dev)
-    ms = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=dev)
-    if world > 1:
-        dist.all_reduce(ms, op=dist.ReduceOp.MAX)
-    ms_iter = float(ms.item()) / args.admm_iters
-    line = {"metric": "ADMM iterations/sec", "value": 1e3 / ms_iter, "unit": "iter/s", "ms_per_iter": ms_iter,
-            "scaling": "strong" if world > 1 else None,  # C5: one fixed grid sharded over N GPUs
-            "iters_timed": args.admm_iters, "warmup_iters": max(3, args.warmup),
-            "config": {"workload": cfg, "n_bus": grid.n_bus, "n_branch": grid.n_branch, "n_gen": grid.n_gen,
-                       "branch_dim": 4, "parallelism": f"branches sharded over {world} GPU(s), NCCL all-gather"},
-            "residuals_first_last": [run.history[0], run.history[-1]]}
-    if world == 1:
-        # C4 with the line limits on (SURVEY §8(f) rank 1): d=6 branch
-        # subproblems + the augmented-Lagrangian rounds inside every iteration
-        ll = A.AdmmSolver(grid, A.AdmmOptions(line_limits=True), local)
-        for _ in range(max(3, args.warmup)):
-            ll.step()
-        r0 = int(ll.get(A.AUGLAG_ROUNDS)[0])
-        k = max(5, args.admm_iters // 2)
+    K = args.admm_iters
+    W0 = max(3, args.warmup)
+
+    def sharded_rate(grid, record):
+        run = A.ShardedAdmm(grid, rank, world, local, record_times=record)
+        for _ in range(W0):
+            run.step()
+        run._ev.clear()
+        stream = torch.cuda.current_stream(dev)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        if world > 1:
+            dist.barrier()
         torch.cuda.synchronize(dev)
-        t0 = time.perf_counter()
-        for _ in range(k):
-            ll.step()
+        e0.record(stream)
+        for _ in range(K):
+            run.step()
+        e1.record(stream)
         torch.cuda.synchronize(dev)
-        dt = (time.perf_counter() - t0) / k
-        line["line_limits"] = {
-            "value": 1.0 / dt, "unit": "iter/s", "ms_per_iter": 1e3 * dt, "iters_timed": k,
-            "auglag_rounds_per_iter": (int(ll.get(A.AUGLAG_ROUNDS)[0]) - r0) / k,
-            "max_line_violation": float(ll.get(A.LINE_VIOL)[0]), "branch_dim": 6,
-            "timing": "host wall clock per blocking tb_admm_step (branch stage = one fused augmented-Lagrangian launch)"}
-        ll.close()
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        ms = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(ms, op=dist.ReduceOp.MAX)
+        return run, float(ms.item()) / K
+
+    c5 = c5_grid()
+    if world > 1:
+        if not dist.is_initialized():
+            return None
+        run, ms_iter = sharded_rate(c5, True)
+        pt = run.partition_times()
+        st = imbalance(pt)
+        return {"metric": "ADMM iterations/sec", "value": 1e3 / ms_iter, "unit": "iter/s", "ms_per_iter": ms_iter,
+                "scaling": "strong", "iters_timed": K, "warmup_iters": W0,
+                "config": {"workload": "C5", "n_bus": c5.n_bus, "n_branch": c5.n_branch, "n_gen": c5.n_gen,
+                           "branch_dim": 4, "parallelism": f"branches sharded over {world} GPUs, NCCL all-gather"},
+                "imbalance": {"nu_max": st.nu_max, "nu_min": st.nu_min, "nu_mean": st.nu_mean,
+                              "partition": "contiguous even (batch.hpp:61-70)",
+                              "stage_ms_per_rank_mean": [1e3 * float(np.mean(c)) for c in zip(*pt)]},
+                "residuals_first_last": [run.history[0], run.history[-1]]}
+
+    # ---- C4 on one GPU
+    grid = synth.grid(13659, 20467, 4092)
+    g_run = A.AdmmSolver(grid, device=local)
+    g_run.run(W0)
+    torch.cuda.synchronize(dev)
+    t0 = time.perf_counter()
+    g_run.run(K)  # max_iter K, no tolerance: exactly K graph-replayed iterations
+    dt_run = (time.perf_counter() - t0) / K
+    g_run.close()
+    step_run, ms_step = sharded_rate(grid, False)
+    line = {"metric": "ADMM iterations/sec", "value": 1.0 / dt_run, "unit": "iter/s", "ms_per_iter": 1e3 * dt_run,
+            "scaling": None, "iters_timed": K, "warmup_iters": W0,
+            "timing": "host wall clock around tb_admm_run(K) (graph replay, one final sync)",
+            "config": {"workload": "C4", "n_bus": grid.n_bus, "n_branch": grid.n_branch, "n_gen": grid.n_gen,
+                       "branch_dim": 4, "parallelism": "1 GPU"},
+            "per_step": {"value": 1e3 / ms_step, "ms_per_iter": ms_step,
+                         "timing": "device events around K blocking sharded-driver steps (residual read-back each)"},
+            "residuals_first_last": [step_run.history[0], step_run.history[-1]]}
+    ll = A.AdmmSolver(grid, A.AdmmOptions(line_limits=True), local)
+    ll.run(W0)
+    r0 = int(ll.get(A.AUGLAG_ROUNDS)[0])
+    k = max(5, K // 2)
+    torch.cuda.synchronize(dev)
+    t0 = time.perf_counter()
+    ll.run(k)
+    dt = (time.perf_counter() - t0) / k
+    line["line_limits"] = {
+        "value": 1.0 / dt, "unit": "iter/s", "ms_per_iter": 1e3 * dt, "iters_timed": k,
+        "auglag_rounds_per_iter": (int(ll.get(A.AUGLAG_ROUNDS)[0]) - r0) / k,
+        "max_line_violation": float(ll.get(A.LINE_VIOL)[0]), "branch_dim": 6,
+        "timing": "host wall clock around tb_admm_run(k) (branch stage = one fused augmented-Lagrangian launch)"}
+    ll.close()
+    if rank == 0 and not args.no_cpu_baseline:
         try:
             from oracle import pyoracle
 
@@ -261,15 +396,26 @@ def run_admm(args, rank, world, local, dev):
             cpu = pyoracle.OracleAdmm(grid, workers=cores)
             cpu.step()
             t0 = time.perf_counter()
-            k = 3
-            for _ in range(k):
+            for _ in range(3):
                 cpu.step()
-            v = k / (time.perf_counter() - t0)
+            v = 3 / (time.perf_counter() - t0)
             line["cpu_baseline"] = {"value": v, "unit": "iter/s", "cores": cores, "kind": "port",
-                                    "sample": f"iterations 2-4 of the same {cfg} ADMM run, oracle/admm_oracle.c "
+                                    "sample": "iterations 2-4 of the same C4 ADMM run, oracle/admm_oracle.c "
                                               f"(branch stage through the C TRON restatement, {cores} threads)"}
         except Exception as e:
             line["cpu_baseline"] = {"value": None, "sample": f"failed: {e}"}
+    # ---- C5 at N = 1 (the first point of the scaling curve) + replayed imbalance
+    c5_run, ms5 = sharded_rate(c5, False)
+    line["c5"] = {"value": 1e3 / ms5, "unit": "iter/s", "ms_per_iter": ms5, "iters_timed": K,
+                  "config": {"workload": "C5", "n_bus": c5.n_bus, "n_branch": c5.n_branch, "n_gen": c5.n_gen,
+                             "parallelism": "1 GPU, sharded driver at world 1"},
+                  "residuals_first_last": [c5_run.history[0], c5_run.history[-1]]}
+    del c5_run
+    if not args.no_imbalance:
+        try:
+            line["c5"]["imbalance_replay"] = replay_imbalance(c5, dev)
+        except Exception as e:
+            line["c5"]["imbalance_replay"] = {"error": repr(e)}
     return line
 
 
@@ -347,6 +493,7 @@ def main():
     ap.add_argument("--no-admm", action="store_true")
     ap.add_argument("--admm-iters", type=int, default=20)
     ap.add_argument("--no-sweep", action="store_true", help="skip the C1 / C3 dimension sweep")
+    ap.add_argument("--no-imbalance", action="store_true", help="skip the replayed C5 partition imbalance")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup) if args.impl == "ours" else args.warmup
 
@@ -530,9 +677,10 @@ def main():
             "gpu_launches": int(launches),
             "parity": parity,
             "status_counts": {str(k): int(v) for k, v in zip(*np.unique(status, return_counts=True))},
-            "admm": admm_line,
+            "admm_detail": sig(admm_line),
             "sweep": sweep,
             "ms_per_step_all": ms_steps,
+            "admm": admm_summary(admm_line),  # last and short: the driver keeps the line's 1,500-char tail
         }
         print(json.dumps(line), flush=True)
     solver.close()
