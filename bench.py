@@ -582,9 +582,32 @@ def main():
     # variant (identical results; the count is deterministic)
     solver.solve_batch(dbatch, cfg=cfg, out=dout, stream=stream.cuda_stream, count_flops=True)
     torch.cuda.synchronize(dev)
-    flops_per_launch = float(dout.flops.sum().item())
+    flops_per_launch = float(dout.flops.sum().item())  # the reference's count (skipped replays credited)
     status = dout.status.cpu().numpy()
-    achieved_tflops = flops_per_launch / (ms_per_step * 1e-3) / 1e12
+    # executed flops: the fast-forwarded replays of a zero-change iteration are
+    # not executed, so they do not count toward the achieved rate
+    exec_solver = Solver((local,), fast_forward=2)
+    exec_solver.solve_batch(dbatch, cfg=cfg, out=dout, stream=stream.cuda_stream, count_flops=True)
+    torch.cuda.synchronize(dev)
+    exec_flops = float(dout.flops.sum().item())
+    exec_solver.close()
+    achieved_tflops = exec_flops / (ms_per_step * 1e-3) / 1e12
+    # the same timed steps with fast-forward off (every replay executed)
+    nff = Solver((local,), fast_forward=False)
+    for _ in range(2):
+        nff.solve_batch(dbatch, cfg=cfg, out=dout, stream=stream.cuda_stream)
+    evn = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    torch.cuda.synchronize(dev)
+    for k in range(args.steps):
+        flush.random_(0, 255)
+        evn[k][0].record(stream)
+        nff.solve_batch(dbatch, cfg=cfg, out=dout, stream=stream.cuda_stream)
+        evn[k][1].record(stream)
+    torch.cuda.synchronize(dev)
+    nff.close()
+    ms_nff = statistics.median(a.elapsed_time(b) for a, b in evn)
+    no_ff = {"value": world * N / (ms_nff * 1e-3), "ms_per_step": ms_nff,
+             "note": "device time with fast_forward off (median step; every zero-change replay executed)"}
     peak = _lib.C.c_double()
     lib.tb_measure_fp64_peak(local, _lib.C.byref(peak))
     fp64_peak = peak.value
@@ -670,8 +693,12 @@ def main():
             "roofline": {"bound": "fp64", "achieved": achieved_tflops, "peak": fp64_peak, "unit": "TFLOP/s",
                          "frac": achieved_tflops / fp64_peak if fp64_peak else None, "traffic": traffic,
                          "peak_source": "DFMA microbenchmark measured in this run (tb_measure_fp64_peak)",
-                         "flops_per_launch": flops_per_launch,
-                         "flop_model": "algorithmic flops per SURVEY 8(d)/DESIGN.md, counted per problem on device"},
+                         "flops_per_launch": exec_flops,
+                         "flops_per_launch_reference_count": flops_per_launch,
+                         "flop_model": "algorithmic flops per SURVEY 8(d)/DESIGN.md, counted per problem on device; "
+                                       "achieved uses the EXECUTED flops (fast-forwarded replays excluded); the "
+                                       "reference count credits them"},
+            "no_fast_forward": no_ff,
             "cpu_baseline": cpu,
             "clocks": clocks.summary(),
             "gpu_launches": int(launches),

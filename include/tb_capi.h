@@ -133,8 +133,11 @@ int64_t tb_family_nparams(int32_t family, int32_t dim);
  * (batch.hpp:61-70). */
 int tb_context_create(const int32_t* devices, int32_t n_devices, tb_context** out);
 int tb_context_destroy(tb_context* ctx);
-/* mode must be TB_MODE_EXACT; fast_forward (default 1) skips the provably
- * identical replays of a rejected zero-change iteration. */
+/* mode must be TB_MODE_EXACT.  fast_forward: 1 (default) skips the provably
+ * identical replays of a rejected zero-change iteration and
+ * credits their flops to the per-problem flop counter (the reference's
+ * count); 2 skips them and counts only the flops executed; 0 replays them.
+ * Every SolveReport field is identical in all three. */
 int tb_context_set_mode(tb_context* ctx, int32_t mode, int32_t fast_forward);
 /* Kernel form (TB_FORM_*, default TB_FORM_AUTO) for the context's later
  * solves; replaces the round-1 TB_THREAD / TB_BLOCK_* environment switches. */

@@ -208,7 +208,8 @@ int tb_context_set_mode(tb_context* ctx, int32_t mode, int32_t fast_forward) {
     if (mode != TB_MODE_EXACT)
         return set_err(TB_E_INVALID_ARGUMENT, "only TB_MODE_EXACT is built in this version");
     ctx->mode = mode;
-    ctx->fast_forward = fast_forward ? 1 : 0;
+    if (fast_forward < 0 || fast_forward > 2) return set_err(TB_E_INVALID_ARGUMENT, "fast_forward must be 0, 1 or 2");
+    ctx->fast_forward = fast_forward;
     return TB_OK;
 }
 

@@ -1223,7 +1223,7 @@ __global__ void __launch_bounds__(D, BlkMinBlocks<D>::value) tron_block_kernel(c
                             cg_iterations += rem * cg_its;
                             f_evals += rem;
                         }
-                        W.count(rem * (W.fl - fl_iter0));
+                        if (a.fast_forward == 1) W.count(rem * (W.fl - fl_iter0));  // 2: executed flops only
                         iterations = cfg.max_iter;
                         break;
                     }
@@ -1265,6 +1265,7 @@ __global__ void __launch_bounds__(D, BlkMinBlocks<D>::value) tron_block_kernel(c
         if (t == 0)
             for (int k = 0; k < 16; ++k) atomicAdd(&g_phase_cycles[k], (unsigned long long)W.ph[k]);
 #endif
+        __syncwarp();  // every lane's last store of the loop scalars before thread 0 reports them
         if (act && a.x_star) a.x_star[pid * n + t] = x;
         if (t == 0) {
             if (a.f_star) a.f_star[pid] = f;

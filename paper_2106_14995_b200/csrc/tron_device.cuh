@@ -589,8 +589,12 @@ struct Warp {
         return trsv_fwd_fn<D, kUnroll>(Lw, RD, b, F, lane);
     }
     __device__ __forceinline__ double trsv_bwd(double b, unsigned F) {
-        double* bb = s2 + tog;  // staging for the non-unrolled variant
-        tog ^= D;
+        // staging for the non-unrolled variant only: the unrolled one neither
+        // stages nor synchronises, so it must not advance the staging toggle
+        // (a toggle without a barrier would let the next staged write reuse a
+        // buffer other lanes may still read: racecheck, r02_sanitize_racecheck)
+        double* bb = s2 + tog;
+        if (!kUnroll) tog ^= D;
         return trsv_bwd_fn<D, kUnroll>(Lw, RD, bb, b, F, lane);
     }
 
@@ -1105,7 +1109,7 @@ __device__ __forceinline__ void tron_solve_one(const KernelArgs& a, const long l
                         cg_iterations += rem * cg_its;
                         f_evals += rem;
                     }
-                    W.count(rem * (W.fl - fl_iter0));
+                    if (a.fast_forward == 1) W.count(rem * (W.fl - fl_iter0));  // 2: executed flops only
                     iterations = cfg.max_iter;
                     break;
                 }
@@ -1149,6 +1153,7 @@ __device__ __forceinline__ void tron_solve_one(const KernelArgs& a, const long l
     if (lane == 0)
         for (int k = 0; k < 8; ++k) atomicAdd(&g_phase_cycles[k], (unsigned long long)W.ph[k]);
 #endif
+    __syncwarp();  // every lane's last store of the loop scalars before lane 0 reports them
     if (act && a.x_star) a.x_star[pid * n + lane] = x;
     if (lane == 0) {
         if (a.f_star) a.f_star[pid] = f;

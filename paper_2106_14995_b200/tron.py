@@ -194,7 +194,7 @@ class Solver:
     """Owns a tb_context (device streams + workspace).  `devices` plays the
     role of solve_batch's `workers`: contiguous even partitions per device."""
 
-    def __init__(self, devices: Sequence[int] = (0,), fast_forward: bool = True,
+    def __init__(self, devices: Sequence[int] = (0,), fast_forward=True,
                  form: "KernelForm" = KernelForm.AUTO):
         self._lib = L.load()
         arr = (C.c_int32 * len(devices))(*devices)
@@ -203,7 +203,8 @@ class Solver:
             raise SolverError(L.last_error())
         self._ctx = ctx
         self.devices = list(devices)
-        if self._lib.tb_context_set_mode(self._ctx, 0, 1 if fast_forward else 0) != L.TB_OK:
+        ff = int(fast_forward) if not isinstance(fast_forward, bool) else (1 if fast_forward else 0)
+        if self._lib.tb_context_set_mode(self._ctx, 0, ff) != L.TB_OK:
             raise SolverError(L.last_error())
         self.set_form(form)
 

@@ -98,3 +98,23 @@ def test_set_form_rejects_unknown():
             s.set_form(2)
     finally:
         s.close()
+
+
+def test_fast_forward_modes_identical_reports():
+    """fast_forward 0 / 1 / 2 (replay / skip + credit the reference's flops /
+    skip + count executed flops): every SolveReport field identical; the
+    credited count equals the replayed count, the executed count is smaller
+    exactly when something was skipped."""
+    b = synth.branch(8192, 6, seed=5)
+    rs = []
+    for ff in (0, 1, 2):
+        s = Solver((0,), fast_forward=ff)
+        try:
+            rs.append(s.solve_batch(b, count_flops=True))
+        finally:
+            s.close()
+    assert_bitwise(rs[1], rs[0], label="ff1 vs ff0")
+    assert_bitwise(rs[2], rs[0], label="ff2 vs ff0")
+    f0, f1, f2 = (host(r.flops) for r in rs)
+    assert np.array_equal(f0, f1)
+    assert (f2 <= f1).all() and (f2 < f1).any()
