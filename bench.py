@@ -644,6 +644,35 @@ def main():
     d2h = (hout.x_star.nbytes + hout.f_star.nbytes + hout.pg_norm.nbytes + hout.status.nbytes +
            hout.iterations.nbytes + hout.cg_iterations.nbytes + hout.f_evals.nbytes + hout.per_problem_time.nbytes)
 
+    # ---- e2e with PAGEABLE host buffers (plain numpy: the library's pinned
+    # staging + chunked pipeline) and through the C++ drop-in
+    # (tronbatch::gpu::solve_batch, std::vector<BranchProblem> in, BatchResult out)
+    pout = Solver.alloc_result(N, DIM, device=False)
+    solver.solve_batch(batch, cfg=cfg, out=pout)
+    pt = []
+    for _ in range(max(3, args.steps // 4)):
+        t0 = time.perf_counter()
+        solver.solve_batch(batch, cfg=cfg, out=pout)
+        pt.append(time.perf_counter() - t0)
+    e2e_pageable = {"value": world * N / statistics.median(pt), "unit": "solves/s",
+                    "note": "same call with pageable numpy buffers (library-owned pinned staging)"}
+    dropin = None
+    exe = os.path.join(ROOT, "oracle", "_ref", "gpu_dropin_bench")
+    if rank == 0 and world == 1 and os.path.exists(exe):
+        try:
+            path = os.path.join("/tmp", f"tb_c2_batch_{os.getpid()}.bin")
+            with open(path, "wb") as fh:
+                fh.write(np.array([N, DIM, batch.params.shape[1]], dtype=np.int64).tobytes())
+                for arr in (batch.x0, batch.lower, batch.upper, batch.params):
+                    fh.write(np.ascontiguousarray(arr, dtype=np.float64).tobytes())
+            out = subprocess.run([exe, path, "5"], capture_output=True, text=True, timeout=300)
+            os.remove(path)
+            dropin = json.loads(out.stdout.strip().splitlines()[-1])
+            dropin["note"] = ("C++ drop-in tronbatch::gpu::solve_batch end to end: vector<BranchProblem> packing, "
+                              "pinned staging, pipeline, 65,536 SolveReports (tests/cpp/gpu_dropin_bench.cpp)")
+        except Exception as e:
+            dropin = {"value": None, "error": repr(e)}
+
     # ---- CPU baseline (rank 0, N=1 only): the reference's solve_batch
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -690,6 +719,8 @@ def main():
             "config": c2_config(N, world),
             "e2e": {"value": e2e_value, "unit": "solves/s", "h2d_bytes_per_step": int(h2d),
                     "d2h_bytes_per_step": int(d2h)},
+            "e2e_pageable": e2e_pageable,
+            "e2e_cpp_dropin": dropin,
             "roofline": {"bound": "fp64", "achieved": achieved_tflops, "peak": fp64_peak, "unit": "TFLOP/s",
                          "frac": achieved_tflops / fp64_peak if fp64_peak else None, "traffic": traffic,
                          "peak_source": "DFMA microbenchmark measured in this run (tb_measure_fp64_peak)",

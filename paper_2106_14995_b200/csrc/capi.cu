@@ -67,6 +67,27 @@ struct DevBuf {
     }
 };
 
+// page-locked host buffer that only grows (library-owned staging for pageable
+// caller buffers)
+struct HostBuf {
+    void* p = nullptr;
+    size_t cap = 0;
+    cudaError_t ensure(size_t bytes) {
+        if (bytes <= cap) return cudaSuccess;
+        if (p) cudaFreeHost(p);  // tb_solve_batch is blocking: no copy is pending
+        p = nullptr;
+        cap = 0;
+        cudaError_t e = cudaHostAlloc(&p, bytes, cudaHostAllocPortable);
+        if (e == cudaSuccess) cap = bytes;
+        return e;
+    }
+    void release() {
+        if (p) cudaFreeHost(p);
+        p = nullptr;
+        cap = 0;
+    }
+};
+
 struct DevState {
     int device = 0;
     cudaStream_t stream = nullptr;
@@ -77,6 +98,8 @@ struct DevState {
     DevBuf out;  // results
     DevBuf flag;
     DevBuf ws;   // block-kernel workspace (d > 16)
+    HostBuf hin;   // pinned staging of pageable inputs (the device `in` layout)
+    HostBuf hout;  // pinned staging of pageable outputs (the device `out` layout)
     // the last launch that used `ws` (block kernel): a later launch on any
     // stream waits for it, so overlapping async solves never share the
     // workspace's work counter and Hessian slices
@@ -197,6 +220,8 @@ int tb_context_destroy(tb_context* ctx) {
         d.out.release();
         d.flag.release();
         d.ws.release();
+        d.hin.release();
+        d.hout.release();
     }
     cudaSetDevice(prev);
     delete ctx;
@@ -494,25 +519,36 @@ extern "C" int tb_solve_batch(tb_context* ctx, const tb_problem_batch* b, const 
         }
     }
 
-    // Pinned host buffers: the partition is cut into chunks, each on its own stream,
+    // Host buffers: the partition is cut into chunks, each on its own stream,
     // so the H2D copy of chunk i+1 and the D2H copy of chunk i-1 overlap the
     // solves, and a long-running problem in one chunk never holds back the
-    // next chunk (warp kernel; the persistent block kernel owns one workspace
-    // per device and runs unchunked).
+    // next chunk (warp / thread kernels; the persistent block kernel owns one
+    // workspace per device and runs unchunked).  Page-locked caller buffers
+    // are copied directly; pageable ones (e.g. the C++ drop-in's vectors) go
+    // through library-owned pinned staging: the host copies chunk i+1's inputs
+    // into it while chunk i solves, and copies chunk i's results out while
+    // later chunks solve.
+    const bool in_pinned = !in_host || (is_pinned(b->x0) && is_pinned(b->lower) && is_pinned(b->upper) &&
+                                        (np == 0 || is_pinned(b->params)));
+    const bool out_pinned =
+        !out_host || (is_pinned(r->x_star) && is_pinned(r->f_star) && is_pinned(r->pg_norm) && is_pinned(r->status) &&
+                      is_pinned(r->iterations) && is_pinned(r->cg_iterations) && is_pinned(r->f_evals) &&
+                      is_pinned(r->wall_time) && is_pinned(r->flops));
+    std::vector<int> nchs(G, 1);
     for (int k = 0; k < G; ++k) {
         DevState& d = ctx->devs[k];
         CUDA_TRY(cudaSetDevice(d.device));
         const int64_t c = cnt[k];
         CUDA_TRY(cudaEventRecord(d.ev[0], d.stream));
-        const bool staged = (in_host || out_host) && c > 0 &&
-                            (!in_host || (is_pinned(b->x0) && is_pinned(b->lower) && is_pinned(b->upper) &&
-                                          (np == 0 || is_pinned(b->params)))) &&
-                            (!out_host || (is_pinned(r->x_star) && is_pinned(r->f_star) && is_pinned(r->status)));
+        const bool staged = (in_host || out_host) && c > 0;  // the host-buffer pipeline
+        const bool in_stage = in_host && !in_pinned && c > 0;
+        const bool out_stage = out_host && !out_pinned && c > 0;
         size_t ws_need = 0;  // > 0: the persistent block kernel (one workspace per device): no chunking
         CUDA_TRY(tbdev::tron_ws_need(b->family, n, c, ctx->form, &ws_need));
         const int nch = (staged && ws_need == 0 && c >= 2 * kChunkMin)
                             ? (int)std::min<int64_t>(max_chunks(true), c / kChunkMin)
                             : 1;
+        nchs[k] = nch;
         if (nch > 1) {
             CUDA_TRY(cudaEventRecord(d.fork, d.stream));
             for (int ch = 0; ch < nch; ++ch) CUDA_TRY(cudaStreamWaitEvent(d.aux[ch], d.fork, 0));
@@ -520,9 +556,19 @@ extern "C" int tb_solve_batch(tb_context* ctx, const tb_problem_batch* b, const 
         const size_t vb = sizeof(double) * (size_t)c * n;
         const size_t pb = sizeof(double) * (size_t)c * stride;
         char* inp = nullptr;
+        char* hinp = nullptr;
         if (in_host && c > 0) {
             CUDA_TRY(d.in.ensure(3 * vb + pb + 64));
             inp = static_cast<char*>(d.in.p);
+            if (in_stage) {
+                CUDA_TRY(d.hin.ensure(3 * vb + pb + 64));
+                hinp = static_cast<char*>(d.hin.p);
+            }
+        }
+        OutPtrs hst{};  // pinned output staging (pageable outputs)
+        if (out_stage) {
+            CUDA_TRY(d.hout.ensure(out_bytes(c, n)));
+            hst = carve(d.hout.p, c, n);
         }
         OutPtrs ofull;
         if (out_host) {
@@ -550,6 +596,20 @@ extern "C" int tb_solve_batch(tb_context* ctx, const tb_problem_batch* b, const 
                 char* dl = inp + vb + sizeof(double) * (size_t)a0 * n;
                 char* du = inp + 2 * vb + sizeof(double) * (size_t)a0 * n;
                 char* dp = inp + 3 * vb + sizeof(double) * (size_t)a0 * stride;
+                if (in_stage) {  // pageable -> pinned staging (host copy), then an async H2D from it
+                    char* hx = hinp + (dx - inp);
+                    char* hl = hinp + (dl - inp);
+                    char* hu = hinp + (du - inp);
+                    char* hp = hinp + (dp - inp);
+                    std::memcpy(hx, x0, cvb);
+                    std::memcpy(hl, lw, cvb);
+                    std::memcpy(hu, up, cvb);
+                    if (cpb) std::memcpy(hp, prm, cpb);
+                    x0 = reinterpret_cast<const double*>(hx);
+                    lw = reinterpret_cast<const double*>(hl);
+                    up = reinterpret_cast<const double*>(hu);
+                    prm = cpb ? reinterpret_cast<const double*>(hp) : nullptr;
+                }
                 CUDA_TRY(cudaMemcpyAsync(dx, x0, cvb, cudaMemcpyHostToDevice, st));
                 CUDA_TRY(cudaMemcpyAsync(dl, lw, cvb, cudaMemcpyHostToDevice, st));
                 CUDA_TRY(cudaMemcpyAsync(du, up, cvb, cudaMemcpyHostToDevice, st));
@@ -572,20 +632,25 @@ extern "C" int tb_solve_batch(tb_context* ctx, const tb_problem_batch* b, const 
             CUDA_TRY(release_ws(d, a, st));
             if (ch == nch - 1 && nch == 1) CUDA_TRY(cudaEventRecord(d.ev[2], st));
             if (out_host && cc > 0) {
-                const int64_t h0 = g0;
+                // pinned caller buffers: straight into them; pageable: into
+                // the pinned staging (copied out after the chunk completes)
+                auto tgt = [&](auto* user, auto* stage, int64_t m) -> decltype(user) {
+                    if (!user) return nullptr;
+                    return out_stage ? stage + a0 * m : user + g0 * m;
+                };
                 auto cp = [&](void* dst, const void* src, size_t bytes) -> cudaError_t {
                     if (!dst) return cudaSuccess;
                     return cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, st);
                 };
-                CUDA_TRY(cp(r->x_star ? r->x_star + h0 * n : nullptr, o.x_star, sizeof(double) * cc * n));
-                CUDA_TRY(cp(r->f_star ? r->f_star + h0 : nullptr, o.f_star, sizeof(double) * cc));
-                CUDA_TRY(cp(r->pg_norm ? r->pg_norm + h0 : nullptr, o.pg, sizeof(double) * cc));
-                CUDA_TRY(cp(r->status ? r->status + h0 : nullptr, o.status, sizeof(int32_t) * cc));
-                CUDA_TRY(cp(r->iterations ? r->iterations + h0 : nullptr, o.iters, sizeof(int32_t) * cc));
-                CUDA_TRY(cp(r->cg_iterations ? r->cg_iterations + h0 : nullptr, o.cg, sizeof(int64_t) * cc));
-                CUDA_TRY(cp(r->f_evals ? r->f_evals + h0 : nullptr, o.fev, sizeof(int64_t) * cc));
-                CUDA_TRY(cp(r->flops ? r->flops + h0 : nullptr, o.flops, sizeof(int64_t) * cc));
-                CUDA_TRY(cp(r->wall_time ? r->wall_time + h0 : nullptr, o.wall, sizeof(double) * cc));
+                CUDA_TRY(cp(tgt(r->x_star, hst.x_star, n), o.x_star, sizeof(double) * cc * n));
+                CUDA_TRY(cp(tgt(r->f_star, hst.f_star, 1), o.f_star, sizeof(double) * cc));
+                CUDA_TRY(cp(tgt(r->pg_norm, hst.pg, 1), o.pg, sizeof(double) * cc));
+                CUDA_TRY(cp(tgt(r->status, hst.status, 1), o.status, sizeof(int32_t) * cc));
+                CUDA_TRY(cp(tgt(r->iterations, hst.iters, 1), o.iters, sizeof(int32_t) * cc));
+                CUDA_TRY(cp(tgt(r->cg_iterations, hst.cg, 1), o.cg, sizeof(int64_t) * cc));
+                CUDA_TRY(cp(tgt(r->f_evals, hst.fev, 1), o.fev, sizeof(int64_t) * cc));
+                CUDA_TRY(cp(tgt(r->flops, hst.flops, 1), o.flops, sizeof(int64_t) * cc));
+                CUDA_TRY(cp(tgt(r->wall_time, hst.wall, 1), o.wall, sizeof(double) * cc));
             }
         }
         if (nch > 1) {  // join the chunk streams back into the partition's stream
@@ -598,6 +663,34 @@ extern "C" int tb_solve_batch(tb_context* ctx, const tb_problem_batch* b, const 
         CUDA_TRY(cudaEventRecord(d.ev[3], d.stream));
     }
 
+    // pageable outputs: copy each chunk out of the pinned staging as soon as
+    // it completes (later chunks keep solving meanwhile)
+    if (out_host && !out_pinned) {
+        for (int k = 0; k < G; ++k) {
+            DevState& d = ctx->devs[k];
+            const int64_t c = cnt[k];
+            if (c == 0) continue;
+            CUDA_TRY(cudaSetDevice(d.device));
+            const OutPtrs hst = carve(d.hout.p, c, n);
+            const int nch = nchs[k];
+            for (int ch = 0; ch < nch; ++ch) {
+                CUDA_TRY(cudaStreamSynchronize(nch > 1 ? d.aux[ch] : d.stream));
+                const int64_t a0 = c * ch / nch, a1 = c * (ch + 1) / nch, cc = a1 - a0, g0 = lo[k] + a0;
+                auto out = [&](auto* user, auto* stage, int64_t m) {
+                    if (user) std::memcpy(user + g0 * m, stage + a0 * m, sizeof(*user) * (size_t)(cc * m));
+                };
+                out(r->x_star, hst.x_star, n);
+                out(r->f_star, hst.f_star, 1);
+                out(r->pg_norm, hst.pg, 1);
+                out(r->status, hst.status, 1);
+                out(r->iterations, hst.iters, 1);
+                out(r->cg_iterations, hst.cg, 1);
+                out(r->f_evals, hst.fev, 1);
+                out(r->flops, hst.flops, 1);
+                out(r->wall_time, hst.wall, 1);
+            }
+        }
+    }
     double kmax = 0.0;
     for (int k = 0; k < G; ++k) {
         DevState& d = ctx->devs[k];

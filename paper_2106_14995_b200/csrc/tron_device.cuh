@@ -819,6 +819,11 @@ struct DevFamily {
     double c0 = 0.0, c1 = 0.0, c2 = 0.0, c3 = 0.0;  // per-lane caches
     tb_branch_ctx* ctx = nullptr;
 
+    // the solver's family interface (tron_solve_one): the per-point context
+    // region in shared memory, and the flop model of the evaluations
+    __device__ __forceinline__ void bind(double* context) { ctx = reinterpret_cast<tb_branch_ctx*>(context); }
+    __device__ __forceinline__ static long long flops(int n, int kind) { return tb_family_flops(FAM, n, kind); }
+
     __device__ __forceinline__ void prepare(Warp<D, COUNT>& W, double x) {
         const int lane = W.lane, n = W.n;
         const bool act = lane < n;
@@ -956,7 +961,10 @@ struct WarpMinBlocks {
 
 // tron.hpp:453-549 solve() of problem `pid` by one warp (the calling warp owns
 // `smem`, SmemLayout<D>::fixed() + params doubles).
-template <int FAM, int D, bool COUNT>
+// FamT: the family's device evaluation (DevFamily for the built-in families;
+// include/tronbatch_gpu/user_family.cuh wraps a caller's own type) with
+// bind / prepare / f / grad / hess / flops.
+template <int FAM, int D, bool COUNT, class FamT = DevFamily<FAM, D, COUNT>>
 __device__ __forceinline__ void tron_solve_one(const KernelArgs& a, const long long pid, double* smem) {
     using SL = SmemLayout<D>;
     const unsigned long long t_start = globaltimer();
@@ -992,8 +1000,8 @@ __device__ __forceinline__ void tron_solve_one(const KernelArgs& a, const long l
         for (int k = lane; k < a.nparams; k += 32) prm_s[k] = gp[k];
     }
     W.prm = prm_s;
-    DevFamily<FAM, D, COUNT> fam;
-    fam.ctx = reinterpret_cast<tb_branch_ctx*>(smem + SL::CTX);
+    FamT fam;
+    fam.bind(smem + SL::CTX);
     const double l = act ? a.lo[pid * n + lane] : 0.0;
     const double u = act ? a.up[pid * n + lane] : 0.0;
     double x = act ? a.x0[pid * n + lane] : 0.0;
@@ -1043,7 +1051,7 @@ __device__ __forceinline__ void tron_solve_one(const KernelArgs& a, const long l
             TB_PH_BEGIN(6)
             fam.prepare(W, xe);
             const double fe = fam.f(W);
-            W.count(tb_family_flops(FAM, n, 0));
+            W.count(FamT::flops(n, 0));
             if (lane == 0) ++f_evals;
             TB_PH_END(W, 6)
             bool take = iter == 0;  // evaluate the gradient at xe
@@ -1085,7 +1093,7 @@ __device__ __forceinline__ void tron_solve_one(const KernelArgs& a, const long l
             }
             if (take) {
                 g = fam.grad(W);  // the context was prepared at xe
-                W.count(tb_family_flops(FAM, n, 1));
+                W.count(FamT::flops(n, 1));
                 pg = W.pgnorm(x, g, l, u);
             }
             if (iter == 0) {
@@ -1120,7 +1128,7 @@ __device__ __forceinline__ void tron_solve_one(const KernelArgs& a, const long l
                 TB_PH_BEGIN(0)
                 fam.hess(W);
                 TB_PH_END(W, 0)
-                W.count(tb_family_flops(FAM, n, 2));
+                W.count(FamT::flops(n, 2));
                 need_hessian = false;
             }
             fl_iter0 = W.fl;

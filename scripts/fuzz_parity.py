@@ -9,7 +9,7 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np  # noqa: E402
 
 from oracle import pyoracle as po  # noqa: E402
-from paper_2106_14995_b200 import ProblemBatch, Solver, TronConfig, synth  # noqa: E402
+from paper_2106_14995_b200 import KernelForm, ProblemBatch, Solver, TronConfig, synth  # noqa: E402
 
 FIELDS = ("x_star", "f_star", "pg_norm", "status", "iterations", "cg_iterations", "f_evals")
 budget = float(sys.argv[1]) if len(sys.argv) > 1 else 300.0
@@ -57,8 +57,14 @@ while time.time() < t_end:
     elif r < 0.55:
         kw = dict(tol_pg=float(10.0 ** rng.uniform(-300, -3)))
     cfg = TronConfig(**kw)
+    # kernel form: AUTO routing, or a forced form where it exists for d
+    forms = [KernelForm.AUTO, KernelForm.WARP] + ([KernelForm.THREAD] if d == 4 and fam in ("ncvx", "branch") else []) \
+        + ([KernelForm.BLOCK] if d >= 9 and fam != "branch" else [])
+    form = forms[int(rng.integers(0, len(forms)))]
+    s.set_form(form)
     try:
-        res = s.solve_batch(b, x0, cfg=cfg)
+        counted = bool(rng.random() < 0.2) and form != KernelForm.THREAD  # the thread form does not count
+        res = s.solve_batch(b, x0, cfg=cfg, count_flops=counted)
         err = None
     except Exception as e:  # the reference would have thrown: compare with the oracle's rc
         res, err = None, e
@@ -68,6 +74,9 @@ while time.time() < t_end:
     if res is None:
         ok = ref.rc != 0
     else:
+        if counted and not np.array_equal(np.asarray(res.flops), ref.flops):
+            ok = False
+            print(f"MISMATCH {fam} d={d} n={n} seed={seed} cfg={kw} form={form.name} field flops", flush=True)
         for k in FIELDS:
             a, c = np.asarray(getattr(res, k)), getattr(ref, k)
             if a.dtype.kind == "f":
@@ -76,7 +85,7 @@ while time.time() < t_end:
                 eq = a == c
             if not eq.all():
                 ok = False
-                print(f"MISMATCH {fam} d={d} n={n} seed={seed} cfg={kw} field {k}", flush=True)
+                print(f"MISMATCH {fam} d={d} n={n} seed={seed} cfg={kw} form={form.name} field {k}", flush=True)
                 break
     if not ok:
         fails += 1
