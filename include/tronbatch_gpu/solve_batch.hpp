@@ -17,11 +17,13 @@
 // plus dim()/lower()/upper() works.
 #pragma once
 
+#include <algorithm>
 #include <cstdint>
 #include <cstring>
 #include <memory>
 #include <stdexcept>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "tronbatch/batch.hpp"
@@ -79,6 +81,25 @@ inline FamilyProblem<TB_FAMILY_HS45> make_hs45(int n, int capacity = kDefaultCap
     return p;
 }
 
+namespace detail {
+// f(begin, end) over contiguous ranges of [0, n) on up to hardware_concurrency
+// host threads (one thread below 8,192 items)
+template <typename F>
+void parallel_ranges(int64_t n, F&& f) {
+    const int64_t hw = std::max<int64_t>(1, std::thread::hardware_concurrency());
+    const int64_t t = std::min<int64_t>(hw, std::max<int64_t>(1, n / 8192));
+    if (t <= 1) {
+        f(int64_t(0), n);
+        return;
+    }
+    std::vector<std::thread> pool;
+    pool.reserve(t - 1);
+    for (int64_t k = 1; k < t; ++k) pool.emplace_back([&, k] { f(n * k / t, n * (k + 1) / t); });
+    f(int64_t(0), n / t);
+    for (auto& th : pool) th.join();
+}
+}  // namespace detail
+
 // ------------------------------------------------------------- context
 class Context {
 public:
@@ -132,17 +153,22 @@ BatchResult solve_batch(const std::vector<P>& problems, const std::vector<Vector
     const int n = problems[0].dim();
     const int64_t np = tb_family_nparams(P::family, n);
     if (np < 0) throw std::invalid_argument("solve_batch: dimension invalid for the problem family");
-    std::vector<double> x0(N * n), lo(N * n), up(N * n), prm(std::max<int64_t>(np, 1) * N);
     for (int64_t i = 0; i < N; ++i) {
         const P& p = problems[i];
         if (p.dim() != n || static_cast<int>(x0s[i].size()) != n || static_cast<int>(p.lower().size()) != n ||
             static_cast<int>(p.upper().size()) != n)
             throw std::invalid_argument("solve: dimension mismatch");
-        std::memcpy(&x0[i * n], x0s[i].data(), sizeof(double) * n);
-        std::memcpy(&lo[i * n], p.lower().data(), sizeof(double) * n);
-        std::memcpy(&up[i * n], p.upper().data(), sizeof(double) * n);
-        if (np > 0) std::memcpy(&prm[i * np], p.params().data(), sizeof(double) * np);
     }
+    std::vector<double> x0(N * n), lo(N * n), up(N * n), prm(std::max<int64_t>(np, 1) * N);
+    detail::parallel_ranges(N, [&](int64_t a, int64_t b) {  // packing: host threads like batch.hpp:61-70
+        for (int64_t i = a; i < b; ++i) {
+            const P& p = problems[i];
+            std::memcpy(&x0[i * n], x0s[i].data(), sizeof(double) * n);
+            std::memcpy(&lo[i * n], p.lower().data(), sizeof(double) * n);
+            std::memcpy(&up[i * n], p.upper().data(), sizeof(double) * n);
+            if (np > 0) std::memcpy(&prm[i * np], p.params().data(), sizeof(double) * np);
+        }
+    });
     tb_problem_batch b{P::family, n, N, x0.data(), lo.data(), up.data(), np > 0 ? prm.data() : nullptr, np,
                        TB_MEM_HOST};
     std::vector<double> xs(N * n), fs(N), pg(N), wt(N);
@@ -170,17 +196,21 @@ BatchResult solve_batch(const std::vector<P>& problems, const std::vector<Vector
     if (rc != TB_OK) throw std::runtime_error(std::string("tronbatch::gpu: ") + tb_last_error());
     out.reports.resize(N);
     out.per_problem_time = wt;
-    for (int64_t i = 0; i < N; ++i) {
-        SolveReport& s = out.reports[i];
-        s.x_star.assign(&xs[i * n], &xs[i * n] + n);
-        s.f_star = fs[i];
-        s.pg_norm = pg[i];
-        s.status = static_cast<SolveStatus>(st[i]);
-        s.iterations = it[i];
-        s.cg_iterations = cg[i];
-        s.f_evals = fe[i];
-        s.wall_time = wt[i];
-    }
+    // one x_star vector per report (the reference's SolveReport): built by
+    // host threads over contiguous ranges (per-thread malloc arenas)
+    detail::parallel_ranges(N, [&](int64_t a, int64_t b) {
+        for (int64_t i = a; i < b; ++i) {
+            SolveReport& s = out.reports[i];
+            s.x_star.assign(&xs[i * n], &xs[i * n] + n);
+            s.f_star = fs[i];
+            s.pg_norm = pg[i];
+            s.status = static_cast<SolveStatus>(st[i]);
+            s.iterations = it[i];
+            s.cg_iterations = cg[i];
+            s.f_evals = fe[i];
+            s.wall_time = wt[i];
+        }
+    });
     out.partition_times.assign(r.partition_times, r.partition_times + r.n_partitions);
     out.batch_wall_time = r.batch_wall_time;
     return out;
