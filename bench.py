@@ -212,12 +212,14 @@ def c5_grid():
 
 def replay_imbalance(grid, dev, iters=5, parts=(2, 4, 8)):
     """SPEC.md:408 / PAPER.md:689-703 per-GPU imbalance of the C5 branch stage
-    at G = 2 / 4 / 8, measured on one GPU: after each ADMM iteration the branch
-    batch (warm starts, current multipliers) is snapshotted and every
-    partition's share is solved alone (its kernel time = what one GPU of a
-    G-GPU run spends on it).  Contiguous even partitions (batch.hpp:61-70, the
-    paper's dispatch) against a cost-aware one (LPT over the per-branch device
-    times of the PREVIOUS iteration's snapshot, PAPER.md:715 future work)."""
+    at G = 2 / 4 / 8, measured on one GPU: before each of `iters` ADMM
+    iterations the branch stage's inputs (warm starts, multipliers) are
+    snapshotted and every partition's share is solved alone
+    (admm.partition_stage_times: its kernel time = what one GPU of a G-GPU run
+    spends on the stage).  Contiguous even partitions (batch.hpp:61-70, the
+    paper's dispatch) against a cost-aware one (LPT over the per-branch TRON
+    iteration counts of the PREVIOUS iteration's stage, PAPER.md:715 future
+    work)."""
     import torch
 
     from paper_2106_14995_b200 import ProblemBatch, Solver, imbalance
@@ -228,33 +230,23 @@ def replay_imbalance(grid, dev, iters=5, parts=(2, 4, 8)):
         run.step()
     solver = Solver((dev.index,))
     n = grid.n_branch
+    lo, up = A.branch_bounds(grid, 4)
     t = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(dev)  # noqa: E731
-    lo = np.stack([grid.bus_vmin[grid.br_from], grid.bus_vmin[grid.br_to], np.full(n, -2 * np.pi),
-                   np.full(n, -2 * np.pi)], axis=1)
-    up = np.stack([grid.bus_vmax[grid.br_from], grid.bus_vmax[grid.br_to], np.full(n, 2 * np.pi),
-                   np.full(n, 2 * np.pi)], axis=1)
-    dlo, dup = t(lo), t(up)
-
-    def part_time(b, idx):
-        sub = ProblemBatch(b.family, 4, b.lower[idx], b.upper[idx], b.params[idx], b.x0[idx])
-        out = Solver.alloc_result(len(idx), 4, device=True)
-        solver.solve_batch(sub, out=out)  # warm-up launch of the same share
-        solver.solve_batch(sub, out=out)
-        return out.kernel_time
-
     prev_cost = None
     times = {("contiguous", G): [] for G in parts}
     times.update({("cost_aware", G): [] for G in parts})
     for _ in range(iters):
-        run.step()
-        b = ProblemBatch(3, 4, dlo, dup, t(run.get(A.BRANCH_PARAMS)), t(run.get(A.BRANCH_X)))
+        x, prm = run.get(A.BRANCH_X), run.get(A.BRANCH_PARAMS)
         full = Solver.alloc_result(n, 4, device=True)
-        solver.solve_batch(b, out=full)
-        cost = full.per_problem_time.cpu().numpy()
+        solver.solve_batch(ProblemBatch(3, 4, t(lo), t(up), t(prm), t(x)), out=full)
+        # cost proxy: TRON iterations per branch (the thread form's per-problem
+        # device time is its whole warp's lifetime, so it does not separate
+        # the branches of one warp)
+        cost = full.iterations.cpu().numpy().astype(np.float64)
         for G in parts:
             cut = [n * k // G for k in range(G + 1)]
-            idx = [torch.arange(cut[k], cut[k + 1], device=dev) for k in range(G)]
-            times[("contiguous", G)].append([part_time(b, i) for i in idx])
+            times[("contiguous", G)].append(A.partition_stage_times(
+                solver, x, prm, lo, up, [np.arange(cut[k], cut[k + 1]) for k in range(G)], dev.index))
             if prev_cost is not None:  # LPT on last iteration's per-branch times
                 order = np.argsort(-prev_cost, kind="stable")
                 load = np.zeros(G)
@@ -263,9 +255,10 @@ def replay_imbalance(grid, dev, iters=5, parts=(2, 4, 8)):
                     k = int(np.argmin(load))
                     owner[j] = k
                     load[k] += prev_cost[j]
-                idx = [torch.from_numpy(np.nonzero(owner == k)[0]).to(dev) for k in range(G)]
-                times[("cost_aware", G)].append([part_time(b, i) for i in idx])
+                times[("cost_aware", G)].append(A.partition_stage_times(
+                    solver, x, prm, lo, up, [np.nonzero(owner == k)[0] for k in range(G)], dev.index))
         prev_cost = cost
+        run.step()
     run.close()
     solver.close()
     out = {}
@@ -277,7 +270,7 @@ def replay_imbalance(grid, dev, iters=5, parts=(2, 4, 8)):
                                                  "max_part_ms": round(1e3 * max(max(r) for r in tt), 3)}
     out["method"] = ("one GPU, each partition's share of the C5 branch stage solved alone (kernel time) on "
                      f"{iters} successive ADMM iterations; cost-aware = LPT over the previous iteration's "
-                     "per-branch device times")
+                     "per-branch TRON iteration counts")
     return out
 
 

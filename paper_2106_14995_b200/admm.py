@@ -248,6 +248,48 @@ class AdmmSolver:
         return out
 
 
+def branch_bounds(grid: Grid, dim: int = 4):
+    """The branch subproblems' bounds (v in [v_min, v_max] of
+    the end buses, theta in [-2 pi, 2 pi]; dim 6 adds the slacks s in
+    [-s-bar^2, 0]) -- the same boxes tb_admm_create builds."""
+    n = grid.n_branch
+    lo = np.stack([grid.bus_vmin[grid.br_from], grid.bus_vmin[grid.br_to], np.full(n, -2 * np.pi),
+                   np.full(n, -2 * np.pi)], 1)
+    up = np.stack([grid.bus_vmax[grid.br_from], grid.bus_vmax[grid.br_to], np.full(n, 2 * np.pi),
+                   np.full(n, 2 * np.pi)], 1)
+    if dim == 6:
+        sm = grid.br_smax2 if grid.br_smax2 is not None else np.full(n, np.inf)
+        lo = np.concatenate([lo, -np.stack([sm, sm], 1)], 1)
+        up = np.concatenate([up, np.zeros((n, 2))], 1)
+    return lo, up
+
+
+def partition_stage_times(solver, x, params, lower, upper, parts, device=0):
+    """Per-partition batch times of one branch stage (SPEC.md:408 history,
+    PAPER.md:689-703): each partition's share of the branch subproblems
+    (`parts`: a list of index arrays, e.g. contiguous even ranges as in
+    batch.hpp:61-70) solved alone on the device from the same warm starts
+    and multipliers the stage used; its kernel time is what one GPU of a
+    len(parts)-GPU run spends on the stage.  `solver`: a tron.Solver."""
+    import torch
+
+    from .tron import ProblemBatch, Solver as _S
+
+    dev = torch.device("cuda", device)
+    t = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(dev)  # noqa: E731
+    dim = x.shape[1]
+    X, P, Lo, Up = t(x), t(params), t(lower), t(upper)
+    out = []
+    for idx in parts:
+        i = torch.as_tensor(np.asarray(idx, dtype=np.int64), device=dev)
+        sub = ProblemBatch(3, dim, Lo[i].contiguous(), Up[i].contiguous(), P[i].contiguous(), X[i].contiguous())
+        res = _S.alloc_result(len(idx), dim, device=True)
+        solver.solve_batch(sub, out=res)  # warm-up launch of the same share
+        solver.solve_batch(sub, out=res)
+        out.append(res.kernel_time)
+    return out
+
+
 def _admm_error(rc: int, msg: str) -> Exception:
     """The reference's exception type for a failed branch solve (batch.hpp:75-76
     rethrows it out of solve_batch, and admm_solve propagates it)."""

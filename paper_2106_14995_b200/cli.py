@@ -8,9 +8,11 @@ bench: solves `batch` copies of hs45(n) on the device; writes bench.csv
 throughput, failures); exit 0 iff every problem converged.
 admm:  parses a MATPOWER case, runs the device ADMM until both residuals meet
 their tolerances or max-iter; writes admm.csv (iter, primal, dual, objective,
-step_time_s) and admm.json (status, iterations, objective, residuals,
-imbalance over the `workers` partitions of the last branch stage); exit 0 iff
-converged, 1 otherwise.  Usage and parse errors exit 2.  Timing columns are the
+step_time_s, stage_time_s and, with --workers G >= 2, batch_time_p0..p{G-1}:
+each contiguous partition's share of that iteration's branch stage solved
+alone, SPEC.md:408) and admm.json (status, iterations, objective, residuals,
+ImbalanceStats over all iterations' partition times); exit 0 iff converged, 1
+otherwise.  Usage and parse errors exit 2.  Timing columns are the
 only non-deterministic outputs.
 """
 from __future__ import annotations
@@ -111,15 +113,33 @@ def run_admm(a) -> int:
     os.makedirs(a.out, exist_ok=True)
     p = d = float("inf")
     k = 0
+    G = a.workers
+    parts = np.array_split(np.arange(case.grid.n_branch), G) if G >= 2 else None
+    lo, up = A.branch_bounds(case.grid, opts.branch_dim)
+    part_times = []  # [iteration][partition] seconds
+    tsolver = None
+    if parts is not None:
+        from . import Solver
+
+        tsolver = Solver((0,))
     with open(os.path.join(a.out, "admm.csv"), "w", newline="") as f:
         w = csv.writer(f)
-        w.writerow(["iter", "primal", "dual", "objective", "step_time_s"])
+        w.writerow(["iter", "primal", "dual", "objective", "step_time_s", "stage_time_s"] +
+                   ([f"batch_time_p{q}" for q in range(G)] if parts is not None else []))
         for k in range(1, a.max_iter + 1):
+            if parts is not None:  # the stage's inputs: warm starts and multipliers before the step
+                x0, prm = solver.get(A.BRANCH_X), solver.get(A.BRANCH_PARAMS)
             t0 = time.perf_counter()
             p, d = solver.step()
             dt = time.perf_counter() - t0
+            stage = solver.stage_times()[0]
             obj = case.cost(solver.get(A.GEN_P))
-            w.writerow([k, repr(p), repr(d), repr(obj), f"{dt:.9f}"])
+            row = [k, repr(p), repr(d), repr(obj), f"{dt:.9f}", f"{stage:.9f}"]
+            if parts is not None:
+                pt = A.partition_stage_times(tsolver, x0, prm, lo, up, parts)
+                part_times.append(pt)
+                row += [f"{v:.9f}" for v in pt]
+            w.writerow(row)
             if p <= a.tol_primal and d <= a.tol_dual:
                 break
     converged = p <= a.tol_primal and d <= a.tol_dual
@@ -129,43 +149,19 @@ def run_admm(a) -> int:
                "line_limits": bool(a.line_limits)}
     if a.line_limits:
         summary["max_line_violation"] = float(solver.get(A.LINE_VIOL)[0])
-    # imbalance (PAPER §5.3) of the last branch stage over `workers` contiguous
-    # partitions, partition time = summed per-branch device time
-    if a.workers >= 2:
-        t = _branch_times(solver, case, opts)
-        parts = np.array_split(t, a.workers)
-        im = imbalance([[float(np.sum(q)) for q in parts]])
+    # ImbalanceStats (batch.hpp:80-111) over every
+    # iteration's per-partition batch times: each contiguous partition's share
+    # of that iteration's branch stage solved alone from the same inputs
+    if part_times:
+        im = imbalance(part_times)
         summary["imbalance"] = {"nu_max": im.nu_max, "nu_min": im.nu_min, "nu_mean": im.nu_mean,
-                                "partitions": a.workers}
+                                "partitions": G, "iterations": len(part_times),
+                                "partition": "contiguous even (batch.hpp:61-70)"}
+        tsolver.close()
     solver.close()
     with open(os.path.join(a.out, "admm.json"), "w") as f:
         json.dump(summary, f, indent=1)
     return EXIT_OK if converged else EXIT_NOT_CONVERGED
-
-
-def _branch_times(solver, case, opts):
-    """Per-branch device times of one more branch solve at the current state."""
-    import numpy as np
-
-    from . import ProblemBatch, Solver
-    from . import admm as A
-
-    g = case.grid
-    D = opts.branch_dim
-    x = solver.get(A.BRANCH_X)
-    prm = solver.get(A.BRANCH_PARAMS)
-    lo = np.stack([g.bus_vmin[g.br_from], g.bus_vmin[g.br_to], np.full(g.n_branch, -2 * np.pi),
-                   np.full(g.n_branch, -2 * np.pi)], 1)
-    up = np.stack([g.bus_vmax[g.br_from], g.bus_vmax[g.br_to], np.full(g.n_branch, 2 * np.pi),
-                   np.full(g.n_branch, 2 * np.pi)], 1)
-    if D == 6:
-        sm = np.where(np.isfinite(prm[:, 35]), prm[:, 35], np.inf)
-        lo = np.concatenate([lo, -np.stack([sm, sm], 1)], 1)
-        up = np.concatenate([up, np.zeros((g.n_branch, 2))], 1)
-    s = Solver((0,))
-    r = s.solve_batch(ProblemBatch(3, D, lo, up, prm, x))
-    s.close()
-    return np.asarray(r.per_problem_time)
 
 
 def main(argv=None) -> int:

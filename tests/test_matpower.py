@@ -188,6 +188,9 @@ def test_cli_bench_and_admm(tmp_path):
     assert r.returncode == 0, r.stderr
     s = json.load(open(tmp_path / "a" / "admm.json"))
     assert s["status"] == "converged" and abs(s["objective"] - 5296.69) <= 1.0 and "imbalance" in s
+    assert s["imbalance"]["partitions"] == 2 and s["imbalance"]["iterations"] == s["iterations"]
+    hdr = open(tmp_path / "a" / "admm.csv").readline().strip().split(",")
+    assert hdr[-3:] == ["stage_time_s", "batch_time_p0", "batch_time_p1"]
     r = _cli("--mode", "admm", "--case", CASE9, "--max-iter", "1", "--out", str(tmp_path / "b"))
     assert r.returncode == 1
     assert len(open(tmp_path / "b" / "admm.csv").read().strip().split("\n")) == 2
