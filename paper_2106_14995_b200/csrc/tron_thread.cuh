@@ -660,12 +660,12 @@ __device__ __forceinline__ void tron_solve_thread(const KernelArgs& a, const lon
 
 // Routing (host): the thread form takes n = 4 batches (the whole batch or
 // partition, not the concurrent chunk) of at least min_count problems: branch
-// 4,096, ncvx 16,384 (TB_THREAD_MIN overrides both).  Measured, device-
+// 4,096, ncvx 16,384 (KernelForm.THREAD forces it).  Measured, device-
 // resident, thread vs warp: ncvx d=4 x32,768 0.95 vs 1.40 ms, x20,467 0.83
 // vs 0.97, x16,384 0.79 vs 0.81, x12,000 0.79 vs 0.66, x1,024 0.70 vs 0.30 (a
 // lone problem's chain is slower on one thread); branch d=4 x65,536 1.12 vs
 // 3.09, x20,467 0.81 vs 1.28, x4,096 0.43 vs 0.57.  At n = 6 / 8 the 255-register thread form loses (7.7 vs 7.4 ms
-// branch6, 13.3 vs 3.6 ms ncvx8).  TB_THREAD=0 forces the warp form.  Flop
+// branch6, 13.3 vs 3.6 ms ncvx8).  KernelForm.WARP forces the warp form.  Flop
 // counting stays in the warp kernel.
 template <int D, int FAM = TB_FAMILY_BRANCH>
 __global__ void __launch_bounds__(64) tron_thread_kernel(const __grid_constant__ KernelArgs a) {
