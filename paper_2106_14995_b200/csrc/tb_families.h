@@ -230,14 +230,20 @@ TB_HD void tb_br_base(const double* x, double* b) {
     b[TB_BRB_WJJ] = vj * vj;
 }
 
-/* F = fa * w_own + fb * wR + fc * wI */
+/* F = fa * w_own + fb * wR + fc * wI:
+ *   f = 0 (p_ij):  gff,  gft,  bft      f = 1 (q_ij): -bff, -bft,  gft
+ *   f = 2 (p_ji):  gtt,  gtf, -btf      f = 3 (q_ji): -btt, -btf, -gtf
+ * Written without a switch (selects on the flow's end and kind: the device
+ * evaluates different flows in different lanes of a warp, where a switch
+ * serialises); negation is exact, so the values are those of the table. */
 TB_HD void tb_br_coef(int f, const double* prm, double* fa, double* fb, double* fc) {
-    switch (f) {
-        case 0: *fa = prm[TB_BR_GFF];  *fb = prm[TB_BR_GFT];  *fc = prm[TB_BR_BFT];  break;
-        case 1: *fa = -prm[TB_BR_BFF]; *fb = -prm[TB_BR_BFT]; *fc = prm[TB_BR_GFT];  break;
-        case 2: *fa = prm[TB_BR_GTT];  *fb = prm[TB_BR_GTF];  *fc = -prm[TB_BR_BTF]; break;
-        default: *fa = -prm[TB_BR_BTT]; *fb = -prm[TB_BR_BTF]; *fc = -prm[TB_BR_GTF]; break;
-    }
+    const int o = f >= 2 ? 4 : 0; /* gtt / btt / gtf / btf sit 4 slots after gff / bff / gft / bft */
+    const int q = f & 1;          /* reactive flow */
+    const double g_own = prm[TB_BR_GFF + o], b_own = prm[TB_BR_BFF + o];
+    const double g_x = prm[TB_BR_GFT + o], b_x = prm[TB_BR_BFT + o];
+    *fa = q ? -b_own : g_own;
+    *fb = q ? -b_x : g_x;
+    *fc = q ? (o ? -g_x : g_x) : (o ? -b_x : b_x);
 }
 
 /* flow f: value, gradient over z, and lam + rho * residual */
@@ -275,24 +281,26 @@ TB_HD void tb_br_line(int l, const double* x, const double* prm, double p, doubl
 }
 
 /* second derivatives of wR and wI at (a, b), a, b < 4 (symmetric) */
+/*   (vi, vj):     cs,          sn              (vi, th_i): -(vj sn),   vj cs
+ *   (vi, th_j):   vj sn,      -(vj cs)         (vj, th_i): -(vi sn),   vi cs
+ *   (vj, th_j):   vi sn,      -(vi cs)         (th_i, th_i), (th_j, th_j): -wR, -wI
+ *   (th_i, th_j): wR,          wI              (vi, vi), (vj, vj): 0, 0
+ * Selects instead of a switch (the device builds the 16 entries in 16 lanes
+ * at once); the same products and exact negations as the table. */
 TB_HD void tb_br_d2w(int a, int b, const double* bs, double* r, double* i) {
     const int lo = a < b ? a : b, hi = a < b ? b : a;
     const double vi = bs[TB_BRB_VI], vj = bs[TB_BRB_VJ], cs = bs[TB_BRB_CS], sn = bs[TB_BRB_SN];
     const double wR = bs[TB_BRB_WR], wI = bs[TB_BRB_WI];
-    double dr = 0.0, di = 0.0;
-    switch (lo * 4 + hi) {
-        case 1: dr = cs; di = sn; break;                      /* (vi, vj) */
-        case 2: dr = -(vj * sn); di = vj * cs; break;         /* (vi, th_i) */
-        case 3: dr = vj * sn; di = -(vj * cs); break;         /* (vi, th_j) */
-        case 6: dr = -(vi * sn); di = vi * cs; break;         /* (vj, th_i) */
-        case 7: dr = vi * sn; di = -(vi * cs); break;         /* (vj, th_j) */
-        case 10: dr = -wR; di = -wI; break;                   /* (th_i, th_i) */
-        case 11: dr = wR; di = wI; break;                     /* (th_i, th_j) */
-        case 15: dr = -wR; di = -wI; break;                   /* (th_j, th_j) */
-        default: break;
-    }
-    *r = dr;
-    *i = di;
+    const int vt = lo < 2 && hi >= 2; /* voltage - angle */
+    const int tt = lo >= 2;           /* angle - angle */
+    const int vv = lo == 0 && hi == 1;
+    const double v = lo == 0 ? vj : vi;
+    const double ps = v * sn, pc = v * cs;
+    const double r0 = vt ? ps : (tt ? wR : (vv ? cs : 0.0));
+    const double i0 = vt ? pc : (tt ? wI : (vv ? sn : 0.0));
+    const int same_angle = tt && lo == hi;
+    *r = ((vt && hi == 2) || same_angle) ? -r0 : r0;
+    *i = ((vt && hi == 3) || same_angle) ? -i0 : i0;
 }
 
 TB_HD double tb_br_d2F(const tb_branch_ctx* c, const double* prm, int f, int a, int b) {
