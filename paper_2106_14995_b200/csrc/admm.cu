@@ -775,9 +775,19 @@ int tb_admm_run(tb_admm* a, int32_t max_iter, double tol_primal, double tol_dual
             cudaGraphExecDestroy(a->graph);
             a->graph = nullptr;
         }
-        a->hist = dalloc<double>(a, (size_t)2 * max_iter, &e);
+        if (a->hist) {  // release the smaller history (no launch uses it any more: the stream is idle)
+            cudaStreamSynchronize(st);
+            a->allocs.erase(std::remove(a->allocs.begin(), a->allocs.end(), static_cast<void*>(a->hist)),
+                            a->allocs.end());
+            cudaFree(a->hist);
+            a->hist = nullptr;
+            a->hist_cap = 0;
+        }
+        // at least 64 iterations so short runs do not rebuild the graph each time
+        const int cap = std::max(max_iter, 64);
+        a->hist = dalloc<double>(a, (size_t)2 * cap, &e);
         if (e != cudaSuccess) return fail(TB_E_CUDA, cudaGetErrorString(e));
-        a->hist_cap = max_iter;
+        a->hist_cap = cap;
     }
     const double tol[2] = {tol_primal, tol_dual};
     e = cudaMemcpyAsync(a->tol, tol, sizeof tol, cudaMemcpyHostToDevice, st);
