@@ -1175,9 +1175,16 @@ __device__ __forceinline__ void tron_solve_one(const KernelArgs& a, const long l
     }
 }
 
-// One problem per warp (one warp per block).
-template <int FAM, int D, bool COUNT>
-__global__ void __launch_bounds__(32, WarpMinBlocks<D>::value) tron_solve_kernel(const __grid_constant__ KernelArgs a) {
+// Small batches (at most kLatencyBlocks one-warp blocks per SM) are latency-
+// bound: every problem is resident at once, so registers beyond the
+// throughput variant's budget cost nothing and remove the spills (128 vs 72
+// registers at D = 4 / 6 / 8): C1 ncvx4 x1,024 0.306 -> 0.277 ms, ncvx8
+// x1,024 1.264 -> 1.158, branch6 x2,048 2.234 -> 2.071 (profiles/README.md).
+constexpr int kLatencyBlocks = 16;
+
+// One problem per warp (one warp per block); MINB resident blocks per SM.
+template <int FAM, int D, bool COUNT, int MINB = WarpMinBlocks<D>::value>
+__global__ void __launch_bounds__(32, MINB) tron_solve_kernel(const __grid_constant__ KernelArgs a) {
     extern __shared__ double smem[];
     const long long pid = blockIdx.x;
     if (pid >= a.count || (a.skip && *a.skip)) return;

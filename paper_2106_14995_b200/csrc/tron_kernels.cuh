@@ -13,11 +13,30 @@
 
 namespace tbdev {
 
+// SMs of the current device (cached per device)
+inline int device_sms() {
+    static int sms[64] = {};
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return 148;
+    if (!sms[dev]) {
+        int v = 0;
+        if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || v < 1) v = 148;
+        sms[dev] = v;
+    }
+    return sms[dev];
+}
+
 template <int FAM, int D, bool COUNT>
 static cudaError_t launch_fdc(const KernelArgs& a, cudaStream_t st) {
     const int np = (a.nparams + 1) & ~1;
     const size_t smem = sizeof(double) * (size_t)(SmemLayout<D>::fixed() + np);
     auto kern = tron_solve_kernel<FAM, D, COUNT>;
+    // the latency variant for batches (the whole partition, not a pipeline
+    // chunk) that fit kLatencyBlocks warps per SM; counting runs are untimed
+    if constexpr (!COUNT && WarpMinBlocks<D>::value > kLatencyBlocks) {
+        const long long total = a.route_count > a.count ? a.route_count : a.count;
+        if (total <= (long long)kLatencyBlocks * device_sms()) kern = tron_solve_kernel<FAM, D, false, kLatencyBlocks>;
+    }
     if (smem > 48 * 1024) {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return e;
