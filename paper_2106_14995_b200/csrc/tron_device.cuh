@@ -314,6 +314,11 @@ struct Warp {
     int tog;        // staging toggle (0 or D)
     unsigned act;   // lanes 0..n-1
     long long fl;   // algorithmic flop counter (tb_flops.h model), COUNT builds only
+    // factor memo (ccf): the free set of the last successful factorization of
+    // the current Hessian, and its flops (COUNT builds)
+    unsigned memo_F;
+    bool memo_ok;
+    long long memo_fl;
     double extrap;  // 1.0 / cfg->interp_factor
 #ifdef TB_PHASES
     long long ph[8];
@@ -536,10 +541,33 @@ struct Warp {
         return winner;
     }
 
+#ifndef TB_CCF_MEMO
+#define TB_CCF_MEMO 1
+#endif
+    // Factor memo: ccf is a pure function of A[F,F].  While the Hessian is
+    // unchanged (rejected steps; hess() clears memo_ok) and the free set
+    // repeats -- the stagnating tail of a solve, repeated faces -- the factor
+    // Lw / RD left by the previous call is the reference's result again (its
+    // shift attempts would replay identically, same flops), so it is reused.
+    // The factor region is written by ccf alone, so Lw / RD are intact.
+    __device__ __forceinline__ int ccf(unsigned F, int nf) {
+        if (TB_CCF_MEMO && memo_ok && F == memo_F) {
+            count(memo_fl);
+            return 0;
+        }
+        const long long fl0 = fl;
+        double shift;
+        const int rc = ccf_compute(F, nf, shift);
+        memo_ok = TB_CCF_MEMO && rc == 0;
+        memo_F = F;
+        if (COUNT) memo_fl = fl - fl0;
+        return rc;
+    }
+
     // dense.hpp:182-201 shifted_factorize on A[F,F].  On success Lw points at
     // the factor and RD holds RN(1 / L(i,i)).  Returns 0 or
     // TB_STATUS_FACTORIZATION_FAILED.
-    __device__ __forceinline__ int ccf(unsigned F, int nf, double& shift) {
+    __device__ __forceinline__ int ccf_compute(unsigned F, int nf, double& shift) {
         const bool inF = lane < D && in_mask(F, lane);
         double dg = inF ? fabs(A[lane + lane * D]) : 0.0;
         if (isnan(dg)) dg = 0.0;
@@ -769,9 +797,8 @@ struct Warp {
             const unsigned F = __ballot_sync(FULL, fr);
             const int nf = __popc(F);
             if (nf == 0) break;
-            double shift;
             TB_PH_BEGIN(2)
-            int rc = ccf(F, nf, shift);
+            int rc = ccf(F, nf);
             TB_PH_END(*this, 2)
             if (rc) return rc;
             const double ldiag = fr ? Lw[lane + lane * D] : 1.0;
@@ -983,6 +1010,9 @@ __device__ __forceinline__ void tron_solve_one(const KernelArgs& a, const long l
     W.tog = 0;
     W.act = (a.n >= 32) ? FULL : ((1u << a.n) - 1u);
     W.fl = 0;
+    W.memo_F = 0;
+    W.memo_ok = false;
+    W.memo_fl = 0;
 #ifdef TB_PHASES
     for (int k = 0; k < 8; ++k) W.ph[k] = 0;
     const long long tb_ph_total0 = clock64();
@@ -1130,6 +1160,7 @@ __device__ __forceinline__ void tron_solve_one(const KernelArgs& a, const long l
                 TB_PH_END(W, 0)
                 W.count(FamT::flops(n, 2));
                 need_hessian = false;
+                W.memo_ok = false;  // a new Hessian: the memoised factor is stale
             }
             fl_iter0 = W.fl;
             __syncwarp();  // every lane has read delta_in / alpha_in (zero-change test)

@@ -231,7 +231,23 @@ struct Th {
         }
         return true;
     }
+    // Factor memo: ccf is a pure function of (A[F,F]); while the Hessian is
+    // unchanged (rejected steps) and the free set repeats -- the stagnating
+    // tail of a solve -- the previous factor is the reference's result again
+    // (its shift attempts replay identically), so it is reused.
+    unsigned memo_F = 0;
+    bool memo_ok = false;
     __device__ __forceinline__ int ccf(unsigned F) {
+#ifndef TB_CCF_MEMO
+#define TB_CCF_MEMO 1
+#endif
+        if (TB_CCF_MEMO && memo_ok && F == memo_F) return 0;
+        const int rc = ccf_compute(F);
+        memo_ok = TB_CCF_MEMO && rc == 0;
+        memo_F = F;
+        return rc;
+    }
+    __device__ __forceinline__ int ccf_compute(unsigned F) {
         double max_diag = 0.0, max_abs = 0.0;
 #pragma unroll
         for (int i = 0; i < D; ++i) {
@@ -628,6 +644,7 @@ __device__ __forceinline__ void tron_solve_thread(const KernelArgs& a, const lon
                         W.A[j + i * D] = h;
                     }
                 need_hessian = false;
+                W.memo_ok = false;  // a new Hessian: the memoised factor is stale
             }
             delta_in = delta;
             alpha_in = alpha_c;
