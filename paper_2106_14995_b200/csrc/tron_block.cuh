@@ -66,15 +66,17 @@ struct BlkLayout {
     static constexpr int S3 = S2 + SW;
     static constexpr int BB = S3 + SW;               // triangular-solve results
     static constexpr int XS = BB + D;                // evaluation point
-    static constexpr int MISC = XS + D;              // 96 doubles of scalars (BM_*)
-    static constexpr int FIDX = MISC + 96;           // D int32: free index by rank
+    static constexpr int MISC = XS + D;              // 104 doubles of scalars (BM_*)
+    static constexpr int FIDX = MISC + 104;          // D int32: free index by rank
     static constexpr int MSK = FIDX + D / 2;         // 2 x NW uint32 ballot words
     static constexpr int AS = MSK + ((NW + 1) & ~1); // Hessian (ASMEM only)
     static constexpr int total() { return AS + (ASMEM ? D * D : 0); }
     static_assert(LP % 2 == 0, "alignment");
 };
 // MISC slots
-enum { BM_RED = 0, BM_PID = 16, BM_GOK = 18, BM_GFL = 22, BM_GRP = 30, BM_PCG = 62, BM_SC = 64, BM_MISC_SIZE = 96 };
+// BM_MEMO: ccf memo -- [0] flag (int), [1] flops (long long), [2..3] free-set ballot words (NW <= 4 uint32)
+enum { BM_RED = 0, BM_PID = 16, BM_GOK = 18, BM_GFL = 22, BM_GRP = 30, BM_PCG = 62, BM_SC = 64, BM_MEMO = 96,
+       BM_MISC_SIZE = 104 };
 
 // a subset of the variables: its size and this thread's ascending rank in it
 // (-1 if absent).  The staged vector of a subset is indexed by rank.
@@ -100,6 +102,7 @@ struct Blk {
     double* misc;
     int* fidx;
     unsigned* msk;
+    const unsigned* cur_mw;  // ballot words of the current free set (build_free_set)
     const double* prm;  // global
     const tb_tron_config* cfg;
     int n;
@@ -332,6 +335,7 @@ struct Blk {
     // ranks the free variables (ascending index), fills fidx / fset / cset
     __device__ __forceinline__ void build_free_set(bool fr) {
         unsigned* mw = msk + (tog ? NW : 0);
+        cur_mw = mw;
         tog ^= D;
         const unsigned b = __ballot_sync(FULL, fr);
         if ((t & 31) == 0) mw[t >> 5] = b;
@@ -448,7 +452,42 @@ struct Blk {
 
     // dense.hpp:182-201 shifted_factorize on B.  On success Lw is the factor
     // and RD its reciprocal diagonal.  Returns 0 or FACTORIZATION_FAILED.
+#ifndef TB_CCF_MEMO
+#define TB_CCF_MEMO 1
+#endif
+    // Factor memo (as in the warp kernel): ccf is a pure function of A[F,F];
+    // while the Hessian is unchanged (the solve loop clears the flag on hess)
+    // and the free set repeats, the factor Lw / RD of the previous call is the
+    // reference's result again (same shift attempts, same flops).  The factor
+    // region is written by ccf alone.  Memo state lives in the block's MISC
+    // slots (written by thread 0 before a barrier, read by every thread).
+    __device__ __forceinline__ bool memo_hit() {
+        const int* flag = reinterpret_cast<const int*>(misc + BM_MEMO);
+        const unsigned* words = reinterpret_cast<const unsigned*>(misc + BM_MEMO + 2);
+        bool hit = *flag != 0;
+#pragma unroll
+        for (int w = 0; w < NW; ++w) hit = hit && words[w] == cur_mw[w];
+        return hit;
+    }
+    __device__ __forceinline__ void memo_store(long long flops) {  // before the barrier that ends ccf
+        if (t == 0) {
+            *reinterpret_cast<int*>(misc + BM_MEMO) = 1;
+            *reinterpret_cast<long long*>(misc + BM_MEMO + 1) = flops;
+            unsigned* words = reinterpret_cast<unsigned*>(misc + BM_MEMO + 2);
+#pragma unroll
+            for (int w = 0; w < NW; ++w) words[w] = cur_mw[w];
+        }
+    }
+    __device__ __forceinline__ void memo_clear() {  // thread 0; ordered by later barriers
+        if (t == 0) *reinterpret_cast<int*>(misc + BM_MEMO) = 0;
+    }
+
     __device__ __forceinline__ int ccf(double& shift) {
+        if (TB_CCF_MEMO && memo_hit()) {
+            count(*reinterpret_cast<const long long*>(misc + BM_MEMO + 1));
+            return 0;
+        }
+        const long long fl0 = fl;
         // 16-lane groups (4 attempts at once) pay at D = 64 (d = 24: -10 %, d = 64: -3 %);
         // at D = 128 eight lockstep groups cost more than they save (+2 %)
         const int gt = (D == 32 && nf <= 8)    ? 8
@@ -524,6 +563,7 @@ struct Blk {
                 shift = sw;
                 Lw = Lbase + winner * lpg;
                 if (t < nf) RD[t] = __drcp_rn(Lat(t, t));
+                if (TB_CCF_MEMO) memo_store(fl - fl0);
                 sync();
                 return 0;
             }
@@ -1113,6 +1153,7 @@ __global__ void __launch_bounds__(D, BlkMinBlocks<D>::value) tron_block_kernel(c
         const long long pid = *pid_slot;
         __syncthreads();
         if (pid >= a.count) break;
+        W.memo_clear();  // a new problem: no memoised factor (ordered by the barriers before ccf)
         const unsigned long long t_start = globaltimer();
         W.fl = 0;
 #ifdef TB_PHASES
@@ -1236,6 +1277,7 @@ __global__ void __launch_bounds__(D, BlkMinBlocks<D>::value) tron_block_kernel(c
                     TB_PH_END(W, 0)
                     W.count(tb_family_flops(FAM, n, 2));
                     need_hessian = false;
+                    W.memo_clear();  // a new Hessian: the memoised factor is stale
                 }
                 fl_iter0 = W.fl;
                 __syncwarp();  // every lane of the warp has read delta_in / alpha_in
