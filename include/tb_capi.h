@@ -136,7 +136,8 @@ int tb_context_destroy(tb_context* ctx);
 /* mode must be TB_MODE_EXACT.  fast_forward: 1 (default) skips the provably
  * identical replays of a rejected zero-change iteration and
  * credits their flops to the per-problem flop counter (the reference's
- * count); 2 skips them and counts only the flops executed; 0 replays them.
+ * count); 2 skips them and counts only the flops executed (also leaving out
+ * the attempts of a memoised factorization); 0 replays them.
  * Every SolveReport field is identical in all three. */
 int tb_context_set_mode(tb_context* ctx, int32_t mode, int32_t fast_forward);
 /* Kernel form (TB_FORM_*, default TB_FORM_AUTO) for the context's later

@@ -103,6 +103,7 @@ struct Blk {
     int* fidx;
     unsigned* msk;
     const unsigned* cur_mw;  // ballot words of the current free set (build_free_set)
+    bool memo_credit;        // credit memoised ccf flops (fast_forward != 2)
     const double* prm;  // global
     const tb_tron_config* cfg;
     int n;
@@ -484,7 +485,7 @@ struct Blk {
 
     __device__ __forceinline__ int ccf(double& shift) {
         if (TB_CCF_MEMO && memo_hit()) {
-            count(*reinterpret_cast<const long long*>(misc + BM_MEMO + 1));
+            if (memo_credit) count(*reinterpret_cast<const long long*>(misc + BM_MEMO + 1));
             return 0;
         }
         const long long fl0 = fl;
@@ -1139,6 +1140,7 @@ __global__ void __launch_bounds__(D, BlkMinBlocks<D>::value) tron_block_kernel(c
     W.tog = 0;
     W.wtog = 0;
     W.nf = 0;
+    W.memo_credit = a.fast_forward != 2;
     const int n = a.n;
     const int t = W.t;
     const bool act = t < n;

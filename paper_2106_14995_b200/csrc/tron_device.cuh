@@ -319,6 +319,7 @@ struct Warp {
     unsigned memo_F;
     bool memo_ok;
     long long memo_fl;
+    bool memo_credit;  // credit a memoised call's flops (fast_forward 1: the reference's count; 2: executed only)
     double extrap;  // 1.0 / cfg->interp_factor
 #ifdef TB_PHASES
     long long ph[8];
@@ -552,7 +553,7 @@ struct Warp {
     // The factor region is written by ccf alone, so Lw / RD are intact.
     __device__ __forceinline__ int ccf(unsigned F, int nf) {
         if (TB_CCF_MEMO && memo_ok && F == memo_F) {
-            count(memo_fl);
+            if (memo_credit) count(memo_fl);
             return 0;
         }
         const long long fl0 = fl;
@@ -1013,6 +1014,7 @@ __device__ __forceinline__ void tron_solve_one(const KernelArgs& a, const long l
     W.memo_F = 0;
     W.memo_ok = false;
     W.memo_fl = 0;
+    W.memo_credit = a.fast_forward != 2;
 #ifdef TB_PHASES
     for (int k = 0; k < 8; ++k) W.ph[k] = 0;
     const long long tb_ph_total0 = clock64();
