@@ -43,7 +43,7 @@ WORKLOAD = "C2: 65,536 synthetic AC-OPF branch augmented-Lagrangian subproblems 
 def kernel_form(d, count):
     """Which device kernel the library routes a (dim, count) ncvx batch to
     under KernelForm.AUTO (csrc/tron_kernels.cuh resolve_form)."""
-    if d == 4 and count >= 16384:
+    if d == 4 and count >= 8192:
         return "thread per problem"
     if d <= 16:
         return "warp per problem"

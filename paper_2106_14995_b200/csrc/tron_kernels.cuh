@@ -145,11 +145,11 @@ inline bool thread_form(const KernelArgs& a, long long min_count) {
 
 // the one routing decision (launchers and tron_form): block kernel for large
 // d, thread form for big n = 4 batches of the families that have it (branch
-// from 4,096 problems, ncvx from 16,384), the warp kernel
+// from 4,096 problems, ncvx from 8,192), the warp kernel
 // otherwise
 inline int resolve_form(int family, const KernelArgs& a) {
     if (family != TB_FAMILY_BRANCH && use_block(a.n, a.form)) return TB_FORM_BLOCK;
-    const long long min_thread = family == TB_FAMILY_BRANCH ? 4096 : (family == TB_FAMILY_NCVX ? 16384 : -1);
+    const long long min_thread = family == TB_FAMILY_BRANCH ? 4096 : (family == TB_FAMILY_NCVX ? 8192 : -1);
     if (thread_form(a, min_thread)) return TB_FORM_THREAD;
     return TB_FORM_WARP;
 }

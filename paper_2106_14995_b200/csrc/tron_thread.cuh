@@ -677,7 +677,8 @@ __device__ __forceinline__ void tron_solve_thread(const KernelArgs& a, const lon
 
 // Routing (host): the thread form takes n = 4 batches (the whole batch or
 // partition, not the concurrent chunk) of at least min_count problems: branch
-// 4,096, ncvx 16,384 (KernelForm.THREAD forces it).  Measured, device-
+// 4,096, ncvx 8,192 (KernelForm.THREAD forces it; round 2, with the factor
+// memo: ncvx4 x8,192 0.471 vs 0.503 ms, x4,096 0.461 vs 0.363).  Round 1, device-
 // resident, thread vs warp: ncvx d=4 x32,768 0.95 vs 1.40 ms, x20,467 0.83
 // vs 0.97, x16,384 0.79 vs 0.81, x12,000 0.79 vs 0.66, x1,024 0.70 vs 0.30 (a
 // lone problem's chain is slower on one thread); branch d=4 x65,536 1.12 vs
