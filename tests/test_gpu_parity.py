@@ -368,16 +368,16 @@ def test_extreme_scales_take_the_ieee_division_path(solver, d, h_scale, c_scale,
 
 
 # ---------------------------------------------------------------- thread form
-# n = 4 batches of >= 4,096 (branch) / 16,384 (ncvx) problems run one thread per
+# n = 4 batches of >= 4,096 (branch) / 8,192 (ncvx) problems run one thread per
 # problem (csrc/tron_thread.cuh); these pin it to the oracle and to the warp
 # form (KernelForm.WARP), also on small batches forced through it
 # (KernelForm.THREAD).
 
 
-@pytest.mark.parametrize("fam,count", [("ncvx", 16384), ("branch", 16384), ("branch", 20467)])
+@pytest.mark.parametrize("fam,count", [("ncvx", 8192), ("ncvx", 16384), ("branch", 16384), ("branch", 20467)])
 def test_thread_form_default_routing_bitwise(solver, monkeypatch, fam, count):
     b = synth.make(fam, count, 4)
-    res = solver.solve_batch(b)  # >= 16,384 / 4,096 problems (whole batch, any chunking): thread form
+    res = solver.solve_batch(b)  # >= 8,192 / 4,096 problems (whole batch, any chunking): thread form
     ref = po.solve_batch(b, impl="oracle", workers=os.cpu_count() or 8)
     assert_bitwise(res, ref, label=f"{fam}4 thread form")
     for form in (KernelForm.WARP,):
