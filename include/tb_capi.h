@@ -167,6 +167,12 @@ const char* tb_last_error(void);
  * scan and ADMM stage kernels; evidence counter for the bench). */
 int64_t tb_kernel_launch_count(void);
 
+/* Page-locked host memory (cudaHostAlloc, portable) for callers that pack
+ * batches themselves (the C++ drop-in): tb_solve_batch copies page-locked
+ * buffers straight into its chunked pipeline, without staging. */
+int tb_host_alloc(int64_t bytes, void** out);
+int tb_host_free(void* p);
+
 /* FP64 DFMA throughput of `device` in TFLOP/s (the roofline denominator of
  * the TRON kernel; measured, not nominal). */
 int tb_measure_fp64_peak(int32_t device, double* tflops);

@@ -112,11 +112,33 @@ public:
     }
     tb_context* get() const { return ctx_.get(); }
 
+    // Page-locked pack / result buffers reused across calls (grown on demand):
+    // the solve copies them straight into its pipeline (no staging, no page
+    // faults of fresh allocations).  A Context is not thread-safe.
+    struct Pinned {
+        void* p = nullptr;
+        size_t cap = 0;
+        ~Pinned() { tb_host_free(p); }
+        void* ensure(size_t bytes) {
+            if (bytes <= cap) return p;
+            tb_host_free(p);
+            p = nullptr;
+            cap = 0;
+            if (tb_host_alloc(static_cast<int64_t>(bytes), &p) != TB_OK)
+                throw std::runtime_error(std::string("tronbatch::gpu: ") + tb_last_error());
+            cap = bytes;
+            return p;
+        }
+    };
+    Pinned& pack() const { return pack_; }
+    Pinned& results() const { return results_; }
+
 private:
     struct Del {
         void operator()(tb_context* c) const { tb_context_destroy(c); }
     };
     std::unique_ptr<tb_context, Del> ctx_;
+    mutable Pinned pack_, results_;
 };
 
 inline tb_tron_config to_c(const TronConfig& cfg) {
@@ -159,8 +181,11 @@ BatchResult solve_batch(const std::vector<P>& problems, const std::vector<Vector
             static_cast<int>(p.upper().size()) != n)
             throw std::invalid_argument("solve: dimension mismatch");
     }
-    std::vector<double> x0(N * n), lo(N * n), up(N * n), prm(std::max<int64_t>(np, 1) * N);
-    detail::parallel_ranges(N, [&](int64_t a, int64_t b) {  // packing: host threads like batch.hpp:61-70
+    // pack into the context's page-locked buffer (host threads like batch.hpp:61-70)
+    const int64_t npk = std::max<int64_t>(np, 1);
+    double* x0 = static_cast<double*>(ctx.pack().ensure(sizeof(double) * size_t(N) * size_t(3 * n + npk)));
+    double *lo = x0 + N * n, *up = lo + N * n, *prm = up + N * n;
+    detail::parallel_ranges(N, [&](int64_t a, int64_t b) {
         for (int64_t i = a; i < b; ++i) {
             const P& p = problems[i];
             std::memcpy(&x0[i * n], x0s[i].data(), sizeof(double) * n);
@@ -169,20 +194,23 @@ BatchResult solve_batch(const std::vector<P>& problems, const std::vector<Vector
             if (np > 0) std::memcpy(&prm[i * np], p.params().data(), sizeof(double) * np);
         }
     });
-    tb_problem_batch b{P::family, n, N, x0.data(), lo.data(), up.data(), np > 0 ? prm.data() : nullptr, np,
-                       TB_MEM_HOST};
-    std::vector<double> xs(N * n), fs(N), pg(N), wt(N);
-    std::vector<int32_t> st(N), it(N);
-    std::vector<int64_t> cg(N), fe(N);
+    tb_problem_batch b{P::family, n, N, x0, lo, up, np > 0 ? prm : nullptr, np, TB_MEM_HOST};
+    // results land in the context's page-locked buffer
+    char* rb = static_cast<char*>(
+        ctx.results().ensure(size_t(N) * (sizeof(double) * (n + 3) + sizeof(int32_t) * 2 + sizeof(int64_t) * 2)));
+    double* xs = reinterpret_cast<double*>(rb);
+    double *fs = xs + N * n, *pg = fs + N, *wt = pg + N;
+    int64_t *cg = reinterpret_cast<int64_t*>(wt + N), *fe = cg + N;
+    int32_t *st = reinterpret_cast<int32_t*>(fe + N), *it = st + N;
     tb_batch_result r{};
-    r.x_star = xs.data();
-    r.f_star = fs.data();
-    r.pg_norm = pg.data();
-    r.status = st.data();
-    r.iterations = it.data();
-    r.cg_iterations = cg.data();
-    r.f_evals = fe.data();
-    r.wall_time = wt.data();
+    r.x_star = xs;
+    r.f_star = fs;
+    r.pg_norm = pg;
+    r.status = st;
+    r.iterations = it;
+    r.cg_iterations = cg;
+    r.f_evals = fe;
+    r.wall_time = wt;
     r.memspace = TB_MEM_HOST;
     const tb_tron_config c = to_c(cfg);
     const int rc = tb_solve_batch(ctx.get(), &b, &c, &r);
@@ -195,7 +223,7 @@ BatchResult solve_batch(const std::vector<P>& problems, const std::vector<Vector
     }
     if (rc != TB_OK) throw std::runtime_error(std::string("tronbatch::gpu: ") + tb_last_error());
     out.reports.resize(N);
-    out.per_problem_time = wt;
+    out.per_problem_time.assign(wt, wt + N);
     // one x_star vector per report (the reference's SolveReport): built by
     // host threads over contiguous ranges (per-thread malloc arenas)
     detail::parallel_ranges(N, [&](int64_t a, int64_t b) {

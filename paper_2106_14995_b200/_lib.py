@@ -109,6 +109,8 @@ SIGNATURES = {
     "tb_last_error": (C.c_char_p, []),
     "tb_kernel_launch_count": (C.c_int64, []),
     "tb_measure_fp64_peak": (C.c_int, [C.c_int32, C.POINTER(C.c_double)]),
+    "tb_host_alloc": (C.c_int, [C.c_int64, C.POINTER(C.c_void_p)]),
+    "tb_host_free": (C.c_int, [C.c_void_p]),
 }
 
 _lib = None

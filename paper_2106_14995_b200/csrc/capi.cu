@@ -238,6 +238,19 @@ int tb_context_set_mode(tb_context* ctx, int32_t mode, int32_t fast_forward) {
     return TB_OK;
 }
 
+int tb_host_alloc(int64_t bytes, void** out) {
+    if (!out || bytes < 0) return set_err(TB_E_INVALID_ARGUMENT, "tb_host_alloc: bad arguments");
+    *out = nullptr;
+    if (bytes == 0) return TB_OK;
+    CUDA_TRY(cudaHostAlloc(out, (size_t)bytes, cudaHostAllocPortable));
+    return TB_OK;
+}
+
+int tb_host_free(void* p) {
+    if (p) CUDA_TRY(cudaFreeHost(p));
+    return TB_OK;
+}
+
 int tb_context_set_form(tb_context* ctx, int32_t form) {
     if (!ctx) return set_err(TB_E_INVALID_ARGUMENT, "null context");
     if (form != TB_FORM_AUTO && form != TB_FORM_WARP && form != TB_FORM_THREAD && form != TB_FORM_BLOCK)
