@@ -37,6 +37,9 @@
 
 #include "tron_device.cuh"
 
+#ifndef TB_HESS_CONST_PART
+#define TB_HESS_CONST_PART 1  // keep the x-independent Hessian part across evaluations (block kernel)
+#endif
 #ifndef TB_BLK_MIN128
 #define TB_BLK_MIN128 4  // resident D = 128 blocks per SM (registers / shared factor region)
 #endif
@@ -1075,7 +1078,12 @@ struct BlkFamily {
         const double e3 = (c0 * c0) * c0;
         return (c1 + k[t] * e3) + a[t] * c3;
     }
-    // row t of the Hessian into A[t + j*D]
+    // row t of the Hessian into A[t + j*D].  The off-diagonal entries of
+    // NCVX (the packed H) and the whole BOXQP Hessian do not depend on x:
+    // after the first evaluation of a problem only the NCVX diagonal is
+    // rewritten (same expressions, same bits; the block's A slice is written
+    // by hess alone, and the family object lives for one problem).
+    bool const_part = false;
     __device__ __forceinline__ void hess(B& W) {
         const int t = W.t, n = W.n;
         const double* prm = W.prm;
@@ -1084,14 +1092,18 @@ struct BlkFamily {
             if (FAM == TB_FAMILY_HS45) {
                 for (int j = 0; j < n; ++j) Ar[j * D] = tb_hs45_hess(W.xs, n, t, j);
             } else if (FAM == TB_FAMILY_BOXQP) {
-                for (int j = 0; j < n; ++j) Ar[j * D] = tb_boxqp_hess(prm, n, t, j);
+                if (!const_part)
+                    for (int j = 0; j < n; ++j) Ar[j * D] = tb_boxqp_hess(prm, n, t, j);
             } else {
                 const double* k = prm + (long)n * (n + 1) / 2 + n;
                 const double* a = k + n;
-                for (int j = 0; j < n; ++j) Ar[j * D] = tb_ncvx_H(prm, n, t, j);
-                Ar[t * D] = (Ar[t * D] + (3.0 * k[t]) * (c0 * c0)) - a[t] * c2;
+                if (!const_part)
+                    for (int j = 0; j < n; ++j)
+                        if (j != t) Ar[j * D] = tb_ncvx_H(prm, n, t, j);
+                Ar[t * D] = (tb_ncvx_H(prm, n, t, t) + (3.0 * k[t]) * (c0 * c0)) - a[t] * c2;
             }
         }
+        const_part = TB_HESS_CONST_PART;
         W.sync();
     }
 };
