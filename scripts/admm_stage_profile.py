@@ -43,3 +43,27 @@ for form in ("THREAD", "WARP"):
         print(f"   branch {i}: {wt[i]*1e3:.3f} ms, {it[i]} iterations, {cg[i]} CG, status {st[i]}, "
               f"{wt[i]/max(it[i],1)*1e6:.2f} us/iteration")
     s.close()
+
+# the long branches alone (what a thread -> warp handoff would leave to a second launch)
+s = Solver((0,), form=KernelForm.THREAD)
+out = Solver.alloc_result(n, 4, device=True)
+s.solve_batch(b, out=out)
+it = out.iterations.cpu().numpy()
+s.close()
+for cut in (16, 32, 64):
+    idx = np.nonzero(it > cut)[0]
+    if len(idx) == 0:
+        continue
+    ti = torch.from_numpy(idx).to(dev)
+    sb = ProblemBatch(3, 4, b.lower[ti].contiguous(), b.upper[ti].contiguous(), b.params[ti].contiguous(),
+                      b.x0[ti].contiguous())
+    for form in ("THREAD", "WARP"):
+        s = Solver((0,), form=KernelForm[form])
+        o = Solver.alloc_result(len(idx), 4, device=True)
+        ts = []
+        for _ in range(5):
+            s.solve_batch(sb, out=o)
+            ts.append(o.kernel_time)
+        print(f"  {len(idx)} branches with > {cut} iterations alone, {form}: {sorted(ts)[2]*1e3:.3f} ms "
+              f"(max iterations {o.iterations.cpu().numpy().max()})")
+        s.close()
