@@ -1,5 +1,6 @@
 """Per-phase share of warp time (debug build with -DTB_PHASES):
-TB_LIB_PATH=scratch_libs/libtb_phases.so python scripts/phase_profile.py branch6 65536"""
+TB_LIB_PATH=scratch_libs/libtb_phases.so python scripts/phase_profile.py branch6 65536
+   [saved.npz: solve that batch (lo, up, prm, x) with the warp form instead]"""
 import ctypes as C, os, sys
 sys.path.insert(0, ".")
 import numpy as np
@@ -8,8 +9,15 @@ from paper_2106_14995_b200 import Solver, _lib, synth
 fam, n = sys.argv[1], int(sys.argv[2])
 name = fam.rstrip("0123456789"); dim = int(fam[len(name):])
 name = {"branch": "branch"}.get(name, name)
-b = synth.make(name, n, dim)
-s = Solver((0,))
+if len(sys.argv) > 3:  # a saved batch (npz with lo, up, prm, x), e.g. the ADMM stage's long branches
+    from paper_2106_14995_b200 import Family, KernelForm, ProblemBatch
+    z = np.load(sys.argv[3])
+    b = ProblemBatch(int(Family[name.upper()]), dim, z["lo"], z["up"], z["prm"], z["x"])
+    n = b.count
+    s = Solver((0,), form=KernelForm.WARP)
+else:
+    b = synth.make(name, n, dim)
+    s = Solver((0,))
 lib = _lib.load()
 rd = getattr(lib, f"tb_debug_read_phases_{name}")
 buf = (C.c_ulonglong * 16)()
