@@ -158,6 +158,25 @@ int tb_solve_batch(tb_context* ctx, const tb_problem_batch* batch, const tb_tron
 int tb_solve_batch_async(tb_context* ctx, const tb_problem_batch* batch, const tb_tron_config* cfg,
                          tb_batch_result* result, void* stream);
 
+/* Per-chunk host callbacks of tb_solve_batch_packed.  `pack` writes problems
+ * [begin, end) into page-locked staging: x0 / lower / upper as
+ * [end - begin][dim], params as [end - begin][nparams] (NULL when the family
+ * has none).  `unpack` receives the results of problems [begin, end) as a host
+ * tb_batch_result whose arrays start at problem `begin` (flops NULL); the
+ * arrays are valid only during the call. */
+typedef void (*tb_pack_fn)(void* user, int64_t begin, int64_t end, double* x0, double* lower, double* upper,
+                           double* params);
+typedef void (*tb_unpack_fn)(void* user, int64_t begin, int64_t end, const tb_batch_result* results);
+/* solve_batch (batch.hpp:27-78) for callers whose problems are not laid out
+ * as arrays (the C++ drop-in's std::vector<P>): the library asks for each
+ * pipeline chunk's inputs just before copying them to the device and hands
+ * over each chunk's results as soon as they arrive, so the caller's packing
+ * and report building overlap the device work on the other chunks.  Errors
+ * as tb_solve_batch; `result` receives the aggregates only.  The callbacks
+ * run on the calling thread, in problem order. */
+int tb_solve_batch_packed(tb_context* ctx, int32_t family, int32_t dim, int64_t count, const tb_tron_config* cfg,
+                          tb_pack_fn pack, tb_unpack_fn unpack, void* user, tb_batch_result* result);
+
 /* imbalance (batch.hpp:89-111): times is [n_iters][n_parts] row-major. */
 int tb_imbalance(const double* times, int32_t n_iters, int32_t n_parts, double* nu_per_iter,
                  double* nu_max, double* nu_min, double* nu_mean);

@@ -18,7 +18,11 @@
 #pragma once
 
 #include <algorithm>
+#include <condition_variable>
 #include <cstdint>
+#include <exception>
+#include <functional>
+#include <mutex>
 #include <cstring>
 #include <memory>
 #include <stdexcept>
@@ -82,28 +86,83 @@ inline FamilyProblem<TB_FAMILY_HS45> make_hs45(int n, int capacity = kDefaultCap
 }
 
 namespace detail {
-// f(begin, end) over contiguous ranges of [0, n) on up to hardware_concurrency
-// host threads (one thread below 8,192 items)
-template <typename F>
-void parallel_ranges(int64_t n, F&& f) {
-    const int64_t hw = std::max<int64_t>(1, std::thread::hardware_concurrency());
-    const int64_t t = std::min<int64_t>(hw, std::max<int64_t>(1, n / 8192));
-    if (t <= 1) {
-        f(int64_t(0), n);
-        return;
+// A fixed pool of host threads owned by the Context: the drop-in packs and
+// unpacks per pipeline chunk, and starting threads for every chunk would cost
+// more than the copies they share.
+class Pool {
+public:
+    explicit Pool(int n) : nt_(std::max(1, n)) {
+        for (int k = 1; k < nt_; ++k) th_.emplace_back([this, k] { loop(k); });
     }
-    std::vector<std::thread> pool;
-    pool.reserve(t - 1);
-    for (int64_t k = 1; k < t; ++k) pool.emplace_back([&, k] { f(n * k / t, n * (k + 1) / t); });
-    f(int64_t(0), n / t);
-    for (auto& th : pool) th.join();
-}
+    ~Pool() {
+        {
+            std::lock_guard<std::mutex> g(m_);
+            stop_ = true;
+            ++gen_;
+        }
+        cv_.notify_all();
+        for (auto& t : th_) t.join();
+    }
+    Pool(const Pool&) = delete;
+    Pool& operator=(const Pool&) = delete;
+
+    // f(begin, end) over contiguous ranges of [0, n), at least `grain` items each
+    template <typename F>
+    void run(int64_t n, int64_t grain, F&& f) {
+        const int64_t t = std::min<int64_t>(nt_, std::max<int64_t>(1, n / std::max<int64_t>(1, grain)));
+        if (t <= 1) {
+            if (n > 0) f(int64_t(0), n);
+            return;
+        }
+        const std::function<void(int)> job = [&](int k) {
+            if (k < t) f(n * k / t, n * (k + 1) / t);
+        };
+        {
+            std::lock_guard<std::mutex> g(m_);
+            job_ = &job;
+            pending_ = nt_ - 1;
+            ++gen_;
+        }
+        cv_.notify_all();
+        job(0);
+        std::unique_lock<std::mutex> l(m_);
+        done_.wait(l, [&] { return pending_ == 0; });
+        job_ = nullptr;
+    }
+
+private:
+    void loop(int k) {
+        uint64_t seen = 0;
+        for (;;) {
+            const std::function<void(int)>* job;
+            {
+                std::unique_lock<std::mutex> l(m_);
+                cv_.wait(l, [&] { return gen_ != seen; });
+                seen = gen_;
+                if (stop_) return;
+                job = job_;
+            }
+            (*job)(k);
+            std::lock_guard<std::mutex> g(m_);
+            if (--pending_ == 0) done_.notify_one();
+        }
+    }
+    int nt_;
+    std::vector<std::thread> th_;
+    std::mutex m_;
+    std::condition_variable cv_, done_;
+    const std::function<void(int)>* job_ = nullptr;
+    uint64_t gen_ = 0;
+    int pending_ = 0;
+    bool stop_ = false;
+};
 }  // namespace detail
 
 // ------------------------------------------------------------- context
 class Context {
 public:
-    explicit Context(const std::vector<int>& devices = {0}) {
+    explicit Context(const std::vector<int>& devices = {0})
+        : pool_(std::make_unique<detail::Pool>(static_cast<int>(std::thread::hardware_concurrency()))) {
         std::vector<int32_t> d(devices.begin(), devices.end());
         tb_context* c = nullptr;
         if (tb_context_create(d.data(), static_cast<int32_t>(d.size()), &c) != TB_OK)
@@ -111,34 +170,15 @@ public:
         ctx_.reset(c);
     }
     tb_context* get() const { return ctx_.get(); }
-
-    // Page-locked pack / result buffers reused across calls (grown on demand):
-    // the solve copies them straight into its pipeline (no staging, no page
-    // faults of fresh allocations).  A Context is not thread-safe.
-    struct Pinned {
-        void* p = nullptr;
-        size_t cap = 0;
-        ~Pinned() { tb_host_free(p); }
-        void* ensure(size_t bytes) {
-            if (bytes <= cap) return p;
-            tb_host_free(p);
-            p = nullptr;
-            cap = 0;
-            if (tb_host_alloc(static_cast<int64_t>(bytes), &p) != TB_OK)
-                throw std::runtime_error(std::string("tronbatch::gpu: ") + tb_last_error());
-            cap = bytes;
-            return p;
-        }
-    };
-    Pinned& pack() const { return pack_; }
-    Pinned& results() const { return results_; }
+    // host threads for packing / report building (a Context is not thread-safe)
+    detail::Pool& pool() const { return *pool_; }
 
 private:
     struct Del {
         void operator()(tb_context* c) const { tb_context_destroy(c); }
     };
     std::unique_ptr<tb_context, Del> ctx_;
-    mutable Pinned pack_, results_;
+    std::unique_ptr<detail::Pool> pool_;
 };
 
 inline tb_tron_config to_c(const TronConfig& cfg) {
@@ -181,39 +221,65 @@ BatchResult solve_batch(const std::vector<P>& problems, const std::vector<Vector
             static_cast<int>(p.upper().size()) != n)
             throw std::invalid_argument("solve: dimension mismatch");
     }
-    // pack into the context's page-locked buffer (host threads like batch.hpp:61-70)
-    const int64_t npk = std::max<int64_t>(np, 1);
-    double* x0 = static_cast<double*>(ctx.pack().ensure(sizeof(double) * size_t(N) * size_t(3 * n + npk)));
-    double *lo = x0 + N * n, *up = lo + N * n, *prm = up + N * n;
-    detail::parallel_ranges(N, [&](int64_t a, int64_t b) {
-        for (int64_t i = a; i < b; ++i) {
-            const P& p = problems[i];
-            std::memcpy(&x0[i * n], x0s[i].data(), sizeof(double) * n);
-            std::memcpy(&lo[i * n], p.lower().data(), sizeof(double) * n);
-            std::memcpy(&up[i * n], p.upper().data(), sizeof(double) * n);
-            if (np > 0) std::memcpy(&prm[i * np], p.params().data(), sizeof(double) * np);
-        }
-    });
-    tb_problem_batch b{P::family, n, N, x0, lo, up, np > 0 ? prm : nullptr, np, TB_MEM_HOST};
-    // results land in the context's page-locked buffer
-    char* rb = static_cast<char*>(
-        ctx.results().ensure(size_t(N) * (sizeof(double) * (n + 3) + sizeof(int32_t) * 2 + sizeof(int64_t) * 2)));
-    double* xs = reinterpret_cast<double*>(rb);
-    double *fs = xs + N * n, *pg = fs + N, *wt = pg + N;
-    int64_t *cg = reinterpret_cast<int64_t*>(wt + N), *fe = cg + N;
-    int32_t *st = reinterpret_cast<int32_t*>(fe + N), *it = st + N;
+    // The library pipelines the batch in chunks: it asks for each chunk's
+    // inputs just before copying them to the device (pack) and hands over
+    // each chunk's results as soon as they arrive (unpack), so packing the
+    // problems and building the SolveReports (host threads, like
+    // batch.hpp:61-70) overlap the device work on the other chunks.
+    out.reports.resize(N);
+    out.per_problem_time.resize(N);
+    struct Job {
+        const std::vector<P>* problems;
+        const std::vector<Vector>* x0s;
+        BatchResult* out;
+        detail::Pool* pool;
+        int n;
+        int64_t np;
+        std::exception_ptr err;
+    } job{&problems, &x0s, &out, &ctx.pool(), n, np, nullptr};
+    constexpr int64_t kGrain = 1024;  // problems per host thread and range
+    const tb_pack_fn pack = [](void* u, int64_t a, int64_t b, double* x0, double* lo, double* up, double* prm) {
+        Job& j = *static_cast<Job*>(u);
+        const int n = j.n;
+        const int64_t np = j.np;
+        j.pool->run(b - a, kGrain, [&](int64_t s, int64_t e) {
+            for (int64_t i = s; i < e; ++i) {
+                const P& p = (*j.problems)[a + i];
+                std::memcpy(&x0[i * n], (*j.x0s)[a + i].data(), sizeof(double) * n);
+                std::memcpy(&lo[i * n], p.lower().data(), sizeof(double) * n);
+                std::memcpy(&up[i * n], p.upper().data(), sizeof(double) * n);
+                if (np > 0) std::memcpy(&prm[i * np], p.params().data(), sizeof(double) * np);
+            }
+        });
+    };
+    const tb_unpack_fn unpack = [](void* u, int64_t a, int64_t b, const tb_batch_result* r) {
+        Job& j = *static_cast<Job*>(u);
+        const int n = j.n;
+        j.pool->run(b - a, kGrain, [&](int64_t s, int64_t e) {
+            try {
+                for (int64_t i = s; i < e; ++i) {
+                    SolveReport& rep = j.out->reports[a + i];
+                    rep.x_star.assign(&r->x_star[i * n], &r->x_star[i * n] + n);
+                    rep.f_star = r->f_star[i];
+                    rep.pg_norm = r->pg_norm[i];
+                    rep.status = static_cast<SolveStatus>(r->status[i]);
+                    rep.iterations = r->iterations[i];
+                    rep.cg_iterations = r->cg_iterations[i];
+                    rep.f_evals = r->f_evals[i];
+                    rep.wall_time = r->wall_time[i];
+                    j.out->per_problem_time[a + i] = r->wall_time[i];
+                }
+            } catch (...) {  // (bad_alloc) never across the C ABI; rethrown below
+                static std::mutex m;
+                std::lock_guard<std::mutex> g(m);
+                if (!j.err) j.err = std::current_exception();
+            }
+        });
+    };
     tb_batch_result r{};
-    r.x_star = xs;
-    r.f_star = fs;
-    r.pg_norm = pg;
-    r.status = st;
-    r.iterations = it;
-    r.cg_iterations = cg;
-    r.f_evals = fe;
-    r.wall_time = wt;
-    r.memspace = TB_MEM_HOST;
     const tb_tron_config c = to_c(cfg);
-    const int rc = tb_solve_batch(ctx.get(), &b, &c, &r);
+    const int rc = tb_solve_batch_packed(ctx.get(), P::family, n, N, &c, pack, unpack, &job, &r);
+    if (job.err) std::rethrow_exception(job.err);
     if (rc == TB_E_INVALID_ARGUMENT) throw std::invalid_argument(tb_last_error());
     if (rc == TB_E_PROBLEM) {
         const std::string msg = tb_last_error();
@@ -222,23 +288,6 @@ BatchResult solve_batch(const std::vector<P>& problems, const std::vector<Vector
         throw std::invalid_argument(msg);
     }
     if (rc != TB_OK) throw std::runtime_error(std::string("tronbatch::gpu: ") + tb_last_error());
-    out.reports.resize(N);
-    out.per_problem_time.assign(wt, wt + N);
-    // one x_star vector per report (the reference's SolveReport): built by
-    // host threads over contiguous ranges (per-thread malloc arenas)
-    detail::parallel_ranges(N, [&](int64_t a, int64_t b) {
-        for (int64_t i = a; i < b; ++i) {
-            SolveReport& s = out.reports[i];
-            s.x_star.assign(&xs[i * n], &xs[i * n] + n);
-            s.f_star = fs[i];
-            s.pg_norm = pg[i];
-            s.status = static_cast<SolveStatus>(st[i]);
-            s.iterations = it[i];
-            s.cg_iterations = cg[i];
-            s.f_evals = fe[i];
-            s.wall_time = wt[i];
-        }
-    });
     out.partition_times.assign(r.partition_times, r.partition_times + r.n_partitions);
     out.batch_wall_time = r.batch_wall_time;
     return out;

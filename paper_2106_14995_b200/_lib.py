@@ -77,6 +77,10 @@ class BatchResultC(C.Structure):
     ]
 
 
+# tb_pack_fn / tb_unpack_fn (tb_solve_batch_packed's per-chunk callbacks)
+PACK_FN = C.CFUNCTYPE(None, C.c_void_p, C.c_int64, C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p)
+UNPACK_FN = C.CFUNCTYPE(None, C.c_void_p, C.c_int64, C.c_int64, C.POINTER(BatchResultC))
+
 # every symbol include/tb_capi.h declares, with its ctypes signature
 SIGNATURES = {
     "tb_config_default": (None, [C.POINTER(TronConfigC)]),
@@ -93,6 +97,11 @@ SIGNATURES = {
     "tb_solve_batch_async": (
         C.c_int,
         [C.c_void_p, C.POINTER(ProblemBatchC), C.POINTER(TronConfigC), C.POINTER(BatchResultC), C.c_void_p],
+    ),
+    "tb_solve_batch_packed": (
+        C.c_int,
+        [C.c_void_p, C.c_int32, C.c_int32, C.c_int64, C.POINTER(TronConfigC), PACK_FN, UNPACK_FN, C.c_void_p,
+         C.POINTER(BatchResultC)],
     ),
     "tb_imbalance": (
         C.c_int,

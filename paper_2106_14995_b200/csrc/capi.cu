@@ -496,8 +496,15 @@ extern "C" int tb_solve_batch_async(tb_context* ctx, const tb_problem_batch* b, 
     return TB_OK;
 }
 
-extern "C" int tb_solve_batch(tb_context* ctx, const tb_problem_batch* b, const tb_tron_config* cfg,
-                              tb_batch_result* r) {
+// tb_solve_batch_packed's callbacks (null for tb_solve_batch)
+struct HostCb {
+    tb_pack_fn pack;
+    tb_unpack_fn unpack;
+    void* user;
+};
+
+static int solve_batch_impl(tb_context* ctx, const tb_problem_batch* b, const tb_tron_config* cfg,
+                            tb_batch_result* r, const HostCb* cb) {
     using clock = std::chrono::steady_clock;
     if (!ctx || !r) return set_err(TB_E_INVALID_ARGUMENT, "solve_batch: null context/result");
     int rc = tb_config_validate(cfg);
@@ -541,12 +548,15 @@ extern "C" int tb_solve_batch(tb_context* ctx, const tb_problem_batch* b, const 
     // through library-owned pinned staging: the host copies chunk i+1's inputs
     // into it while chunk i solves, and copies chunk i's results out while
     // later chunks solve.
-    const bool in_pinned = !in_host || (is_pinned(b->x0) && is_pinned(b->lower) && is_pinned(b->upper) &&
-                                        (np == 0 || is_pinned(b->params)));
+    // callbacks: the caller packs into / unpacks from the pinned staging
+    const bool in_pinned = !cb && (!in_host || (is_pinned(b->x0) && is_pinned(b->lower) && is_pinned(b->upper) &&
+                                                (np == 0 || is_pinned(b->params))));
     const bool out_pinned =
-        !out_host || (is_pinned(r->x_star) && is_pinned(r->f_star) && is_pinned(r->pg_norm) && is_pinned(r->status) &&
-                      is_pinned(r->iterations) && is_pinned(r->cg_iterations) && is_pinned(r->f_evals) &&
-                      is_pinned(r->wall_time) && is_pinned(r->flops));
+        !cb && (!out_host || (is_pinned(r->x_star) && is_pinned(r->f_star) && is_pinned(r->pg_norm) &&
+                              is_pinned(r->status) && is_pinned(r->iterations) && is_pinned(r->cg_iterations) &&
+                              is_pinned(r->f_evals) && is_pinned(r->wall_time) && is_pinned(r->flops)));
+    int64_t first_bad = -1;  // first problem the reference would have thrown on (batch.hpp:75-76)
+    int bad_status = 0;
     std::vector<int> nchs(G, 1);
     for (int k = 0; k < G; ++k) {
         DevState& d = ctx->devs[k];
@@ -601,8 +611,9 @@ extern "C" int tb_solve_batch(tb_context* ctx, const tb_problem_batch* b, const 
             cudaStream_t st = nch > 1 ? d.aux[ch] : d.stream;
             const int64_t a0 = c * ch / nch, a1 = c * (ch + 1) / nch, cc = a1 - a0;  // local range
             const int64_t g0 = lo[k] + a0;                                             // global index
-            const double *x0 = b->x0 + g0 * n, *lw = b->lower + g0 * n, *up = b->upper + g0 * n;
-            const double* prm = np > 0 ? b->params + g0 * stride : nullptr;
+            const double *x0 = cb ? nullptr : b->x0 + g0 * n, *lw = cb ? nullptr : b->lower + g0 * n,
+                         *up = cb ? nullptr : b->upper + g0 * n;
+            const double* prm = (np > 0 && !cb) ? b->params + g0 * stride : nullptr;
             if (in_host && cc > 0) {
                 const size_t cvb = sizeof(double) * (size_t)cc * n, cpb = sizeof(double) * (size_t)cc * stride;
                 char* dx = inp + sizeof(double) * (size_t)a0 * n;
@@ -614,10 +625,15 @@ extern "C" int tb_solve_batch(tb_context* ctx, const tb_problem_batch* b, const 
                     char* hl = hinp + (dl - inp);
                     char* hu = hinp + (du - inp);
                     char* hp = hinp + (dp - inp);
-                    std::memcpy(hx, x0, cvb);
-                    std::memcpy(hl, lw, cvb);
-                    std::memcpy(hu, up, cvb);
-                    if (cpb) std::memcpy(hp, prm, cpb);
+                    if (cb) {
+                        cb->pack(cb->user, g0, g0 + cc, reinterpret_cast<double*>(hx), reinterpret_cast<double*>(hl),
+                                 reinterpret_cast<double*>(hu), cpb ? reinterpret_cast<double*>(hp) : nullptr);
+                    } else {
+                        std::memcpy(hx, x0, cvb);
+                        std::memcpy(hl, lw, cvb);
+                        std::memcpy(hu, up, cvb);
+                        if (cpb) std::memcpy(hp, prm, cpb);
+                    }
                     x0 = reinterpret_cast<const double*>(hx);
                     lw = reinterpret_cast<const double*>(hl);
                     up = reinterpret_cast<const double*>(hu);
@@ -648,11 +664,11 @@ extern "C" int tb_solve_batch(tb_context* ctx, const tb_problem_batch* b, const 
                 // pinned caller buffers: straight into them; pageable: into
                 // the pinned staging (copied out after the chunk completes)
                 auto tgt = [&](auto* user, auto* stage, int64_t m) -> decltype(user) {
-                    if (!user) return nullptr;
+                    if (!user && !(cb && stage)) return nullptr;  // callbacks: every report field
                     return out_stage ? stage + a0 * m : user + g0 * m;
                 };
                 auto cp = [&](void* dst, const void* src, size_t bytes) -> cudaError_t {
-                    if (!dst) return cudaSuccess;
+                    if (!dst || !src) return cudaSuccess;
                     return cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, st);
                 };
                 CUDA_TRY(cp(tgt(r->x_star, hst.x_star, n), o.x_star, sizeof(double) * cc * n));
@@ -689,6 +705,25 @@ extern "C" int tb_solve_batch(tb_context* ctx, const tb_problem_batch* b, const 
             for (int ch = 0; ch < nch; ++ch) {
                 CUDA_TRY(cudaStreamSynchronize(nch > 1 ? d.aux[ch] : d.stream));
                 const int64_t a0 = c * ch / nch, a1 = c * (ch + 1) / nch, cc = a1 - a0, g0 = lo[k] + a0;
+                if (cb) {  // the chunk's reports, straight from the staging
+                    for (int64_t i = 0; i < cc && first_bad < 0; ++i)
+                        if (hst.status[a0 + i] >= TB_STATUS_EVALUATION_ERROR) {
+                            first_bad = g0 + i;
+                            bad_status = hst.status[a0 + i];
+                        }
+                    tb_batch_result v{};
+                    v.x_star = hst.x_star + a0 * n;
+                    v.f_star = hst.f_star + a0;
+                    v.pg_norm = hst.pg + a0;
+                    v.status = hst.status + a0;
+                    v.iterations = hst.iters + a0;
+                    v.cg_iterations = hst.cg + a0;
+                    v.f_evals = hst.fev + a0;
+                    v.wall_time = hst.wall + a0;
+                    v.memspace = TB_MEM_HOST;
+                    if (cc > 0) cb->unpack(cb->user, g0, g0 + cc, &v);
+                    continue;
+                }
                 auto out = [&](auto* user, auto* stage, int64_t m) {
                     if (user) std::memcpy(user + g0 * m, stage + a0 * m, sizeof(*user) * (size_t)(cc * m));
                 };
@@ -719,10 +754,9 @@ extern "C" int tb_solve_batch(tb_context* ctx, const tb_problem_batch* b, const 
     r->batch_wall_time = std::chrono::duration<double>(clock::now() - t0).count();
 
     // batch.hpp:75-76: the first problem (input order) the reference would
-    // have thrown on turns the whole call into an error.
-    int64_t first_bad = -1;
-    int bad_status = 0;
-    for (int k = 0; k < G && first_bad < 0; ++k) {
+    // have thrown on turns the whole call into an error (callbacks: found
+    // while unpacking).
+    for (int k = 0; k < G && first_bad < 0 && !cb; ++k) {
         const int64_t c = cnt[k];
         if (c == 0) continue;
         DevState& d = ctx->devs[k];
@@ -758,4 +792,30 @@ extern "C" int tb_solve_batch(tb_context* ctx, const tb_problem_batch* b, const 
     if (first_bad >= 0)
         return set_err(TB_E_PROBLEM, "problem %lld: %s", (long long)first_bad, status_message(bad_status));
     return TB_OK;
+}
+
+extern "C" int tb_solve_batch(tb_context* ctx, const tb_problem_batch* b, const tb_tron_config* cfg,
+                              tb_batch_result* r) {
+    return solve_batch_impl(ctx, b, cfg, r, nullptr);
+}
+
+extern "C" int tb_solve_batch_packed(tb_context* ctx, int32_t family, int32_t dim, int64_t count,
+                                     const tb_tron_config* cfg, tb_pack_fn pack, tb_unpack_fn unpack, void* user,
+                                     tb_batch_result* r) {
+    if (!pack || !unpack) return set_err(TB_E_INVALID_ARGUMENT, "solve_batch_packed: null pack/unpack callback");
+    if (!r) return set_err(TB_E_INVALID_ARGUMENT, "solve_batch: null context/result");
+    // the batch's arrays are never read (the callbacks fill the staging);
+    // non-null placeholders satisfy the argument checks
+    static double placeholder;
+    tb_problem_batch b{family, dim, count, &placeholder, &placeholder, &placeholder, &placeholder,
+                       tb_family_nparams(family, dim) > 0 ? tb_family_nparams(family, dim) : 0, TB_MEM_HOST};
+    tb_batch_result agg{};
+    agg.memspace = TB_MEM_HOST;
+    const HostCb cb{pack, unpack, user};
+    const int rc = solve_batch_impl(ctx, &b, cfg, &agg, &cb);
+    std::memcpy(r->partition_times, agg.partition_times, sizeof agg.partition_times);
+    r->n_partitions = agg.n_partitions;
+    r->batch_wall_time = agg.batch_wall_time;
+    r->kernel_time = agg.kernel_time;
+    return rc;
 }
