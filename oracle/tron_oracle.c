@@ -136,6 +136,10 @@ int orc_chol_right(int n, const double* A, double shift, double* L) {
  * up to cap = 1e8 * max(1, max_abs(A)) */
 /* diagnostics: histogram of attempts per shifted_factorize call */
 static long g_ccf_hist[64];
+/* the device's closed form of t shift-escalation steps (tb_math.h), for the
+ * CPU test that pins it to the reference's iteration (dense.hpp:197) */
+double orc_debug_shift_ahead(double a, double alpha0, int t) { return tb_shift_ahead(a, alpha0, t); }
+
 void orc_debug_ccf_hist(long* out, int clear) {
     for (int k = 0; k < 64; ++k) {
         out[k] = __atomic_load_n(&g_ccf_hist[k], __ATOMIC_RELAXED);

@@ -27,6 +27,26 @@
 TB_HD double tb_smax(double a, double b) { return (a < b) ? b : a; }
 TB_HD double tb_smin(double a, double b) { return (b < a) ? b : a; }
 
+/* 2^t for 0 <= t <= 1023, exact */
+TB_HD double tb_pow2(int t) {
+    union {
+        unsigned long long u;
+        double d;
+    } v;
+    v.u = (unsigned long long)(1023 + t) << 52;
+    return v.d;
+}
+
+/* t steps of the shift escalation a <- std::max(2 a, alpha0) (dense.hpp:197)
+ * at once, for a >= 0 and alpha0 > 0 (0 <= t <= 1000): doubling is exact
+ * and std::max returns one of its operands, so by induction the t-th iterate
+ * is max(2^t a, 2^(t-1) alpha0) bit for bit (an overflow gives inf both
+ * ways).  Takes the shift of a parallel attempt group off a serial chain. */
+TB_HD double tb_shift_ahead(double a, double alpha0, int t) {
+    const double s = tb_smax(a * tb_pow2(t), alpha0 * tb_pow2(t > 0 ? t - 1 : 0));
+    return t > 0 ? s : a;  // a select: t differs between the lane groups of a warp
+}
+
 /* fdlibm-style Cody-Waite reduction by pi/2 (33-bit head + tail) and the
  * fdlibm minimax kernels on [-pi/4, pi/4].  Accurate to ~1 ulp for |x| < 1e5,
  * deterministic everywhere; returns NaN for non-finite input. */

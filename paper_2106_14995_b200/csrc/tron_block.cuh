@@ -528,8 +528,7 @@ struct Blk {
         double base = 0.0;  // a_{k0}
 #pragma unroll 1
         for (int k0 = 0;; k0 += G) {
-            double sh = base;
-            for (int q = 0; q < gid; ++q) sh = tb_smax(2.0 * sh, alpha0);
+            const double sh = tb_shift_ahead(base, alpha0, gid);  // a_{k0+gid}
             const bool valid = (k0 + gid == 0) || (sh <= cap);
             long long fla = 0;
             bool ok = false, bad = false;
@@ -562,9 +561,7 @@ struct Blk {
                     if (gok[q] >= 0) count(gfl[q] + ((q < winner || winner < 0) ? 1 : 0));
             }
             if (winner >= 0) {
-                double sw = base;
-                for (int q = 0; q < winner; ++q) sw = tb_smax(2.0 * sw, alpha0);
-                shift = sw;
+                shift = tb_shift_ahead(base, alpha0, winner);
                 Lw = Lbase + winner * lpg;
                 if (t < nf) RD[t] = __drcp_rn(Lat(t, t));
                 if (TB_CCF_MEMO) memo_store(fl - fl0);
@@ -574,7 +571,7 @@ struct Blk {
             // no success among attempts k0..k0+G-1: the reference throws at
             // the first a_k > cap (all earlier attempts failed)
             if (!all_valid) return TB_STATUS_FACTORIZATION_FAILED;
-            for (int q = 0; q < G; ++q) base = tb_smax(2.0 * base, alpha0);
+            base = tb_shift_ahead(base, alpha0, G);
             sync();  // gok / group slots are rewritten by the next round
         }
     }

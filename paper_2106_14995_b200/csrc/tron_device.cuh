@@ -588,8 +588,9 @@ struct Warp {
         double base = 0.0;  // a_{k0}
 #pragma unroll 1
         for (int k0 = 0; k0 < 4096; k0 += G) {
-            double sh = base;
-            for (int t = 0; t < g; ++t) sh = tb_smax(2.0 * sh, alpha0);
+            // a_{k0+g}: closed form (tb_math.h); at G = 2 the single step
+            // (D = 16: the closed form measured 1.6 % slower there)
+            const double sh = G <= 2 ? (g ? tb_smax(2.0 * base, alpha0) : base) : tb_shift_ahead(base, alpha0, g);
             const bool valid = (k0 + g == 0) || (sh <= cap);
             long long flr = 0;
             const int w = chol_round(F, nf, sh, valid, flr);
@@ -607,7 +608,11 @@ struct Warp {
             // no success among attempts k0..k0+G-1: the reference throws at
             // the first a_k > cap (all earlier attempts failed)
             if (!__all_sync(FULL, valid)) return TB_STATUS_FACTORIZATION_FAILED;
-            for (int t = 0; t < G; ++t) base = tb_smax(2.0 * base, alpha0);
+            if (G <= 2) {
+                for (int t = 0; t < G; ++t) base = tb_smax(2.0 * base, alpha0);
+            } else {
+                base = tb_shift_ahead(base, alpha0, G);
+            }
         }
         // unreachable for finite data (alpha doubles past any finite cap);
         // with an infinite cap the reference never terminates
