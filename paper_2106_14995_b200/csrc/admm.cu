@@ -44,7 +44,10 @@ __global__ void admm_gen_kernel(tb_admm_view v, const int* stop) {
 // one branch TRON solve per thread (tron_thread.cuh; in place: each thread
 // reads its x0 before it writes x*).  The stages touch disjoint state.
 constexpr int kThreadBlock = 64;
-__global__ void __launch_bounds__(kThreadBlock)
+#ifndef TB_ADMM_BRANCH_MINB
+#define TB_ADMM_BRANCH_MINB 1  // resident 64-thread blocks per SM the register budget must allow
+#endif
+__global__ void __launch_bounds__(kThreadBlock, TB_ADMM_BRANCH_MINB)
     admm_gen_branch_kernel(const __grid_constant__ tbdev::KernelArgs k, tb_admm_view v, int gen_blocks) {
     if (stopped(k.skip)) return;
     if ((int)blockIdx.x < gen_blocks) {
