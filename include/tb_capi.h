@@ -63,6 +63,18 @@ extern "C" {
 #define TB_FORM_THREAD 3 /* one thread per problem, d = 4 */
 #define TB_FORM_BLOCK 4  /* 32 / 64 / 128 threads per problem, persistent, d >= 9 */
 
+/* Launch order of a batch (tb_context_set_order).  Results never depend on
+ * it (each problem is solved independently and reported at its own index);
+ * it decides which problems start first.  START_PG launches the problems in
+ * descending projected-gradient norm at their clipped start points, the
+ * quantity solve() tests first and a good predictor of the iterations a
+ * problem needs, so the long solves start early instead of forming the
+ * launch's tail.  AUTO uses it where it was measured to pay
+ * (one-warp-per-problem launches larger than one wave), INDEX never. */
+#define TB_ORDER_AUTO 0
+#define TB_ORDER_INDEX 1
+#define TB_ORDER_START_PG 2
+
 /* TronConfig (tron.hpp:54-81), field for field; std::optional delta0 becomes
  * has_delta0 + delta0. */
 typedef struct tb_tron_config {
@@ -143,6 +155,9 @@ int tb_context_set_mode(tb_context* ctx, int32_t mode, int32_t fast_forward);
 /* Kernel form (TB_FORM_*, default TB_FORM_AUTO) for the context's later
  * solves; replaces the round-1 TB_THREAD / TB_BLOCK_* environment switches. */
 int tb_context_set_form(tb_context* ctx, int32_t form);
+/* Launch order (TB_ORDER_*, default TB_ORDER_AUTO) for the context's later
+ * solves. */
+int tb_context_set_order(tb_context* ctx, int32_t order);
 
 /* solve_batch (batch.hpp:27-78): blocking.  Returns TB_E_PROBLEM if any
  * problem reports a status >= TB_STATUS_EVALUATION_ERROR (the reference would

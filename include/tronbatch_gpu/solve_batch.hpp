@@ -30,6 +30,10 @@
 #include <thread>
 #include <vector>
 
+#if defined(__SSE2__)
+#include <emmintrin.h>
+#endif
+
 #include "tronbatch/batch.hpp"
 #include "tronbatch/tron.hpp"
 
@@ -86,6 +90,23 @@ inline FamilyProblem<TB_FAMILY_HS45> make_hs45(int n, int capacity = kDefaultCap
 }
 
 namespace detail {
+// Copy `count` doubles into the library's page-locked staging with streaming
+// stores: a transfer of lines the CPU just wrote normally (dirty in its
+// caches) runs at a third of the link rate (host buffers).
+inline void stage_copy(double* dst, const double* src, std::size_t count) {
+#if defined(__SSE2__)
+    std::size_t i = 0;
+    if (reinterpret_cast<std::uintptr_t>(dst) & 15) {
+        dst[0] = src[0];
+        i = 1;
+    }
+    for (; i + 2 <= count; i += 2) _mm_stream_pd(dst + i, _mm_loadu_pd(src + i));
+    if (i < count) dst[i] = src[i];
+#else
+    std::memcpy(dst, src, sizeof(double) * count);
+#endif
+}
+
 // A fixed pool of host threads owned by the Context: the drop-in packs and
 // unpacks per pipeline chunk, and starting threads for every chunk would cost
 // more than the copies they share.
@@ -226,17 +247,29 @@ BatchResult solve_batch(const std::vector<P>& problems, const std::vector<Vector
     // each chunk's results as soon as they arrive (unpack), so packing the
     // problems and building the SolveReports (host threads, like
     // batch.hpp:61-70) overlap the device work on the other chunks.
-    out.reports.resize(N);
+    // The SolveReports (one heap vector each) are allocated on a helper
+    // thread while the device works; the first unpack waits for it.
     out.per_problem_time.resize(N);
+    std::exception_ptr prep_err;
+    std::thread prep([&] {
+        try {
+            out.reports.resize(N);
+            for (SolveReport& rep : out.reports) rep.x_star.resize(n);
+        } catch (...) {
+            prep_err = std::current_exception();
+        }
+    });
     struct Job {
         const std::vector<P>* problems;
         const std::vector<Vector>* x0s;
         BatchResult* out;
         detail::Pool* pool;
+        std::thread* prep;
+        std::exception_ptr* prep_err;
         int n;
         int64_t np;
         std::exception_ptr err;
-    } job{&problems, &x0s, &out, &ctx.pool(), n, np, nullptr};
+    } job{&problems, &x0s, &out, &ctx.pool(), &prep, &prep_err, n, np, nullptr};
     constexpr int64_t kGrain = 1024;  // problems per host thread and range
     const tb_pack_fn pack = [](void* u, int64_t a, int64_t b, double* x0, double* lo, double* up, double* prm) {
         Job& j = *static_cast<Job*>(u);
@@ -245,21 +278,26 @@ BatchResult solve_batch(const std::vector<P>& problems, const std::vector<Vector
         j.pool->run(b - a, kGrain, [&](int64_t s, int64_t e) {
             for (int64_t i = s; i < e; ++i) {
                 const P& p = (*j.problems)[a + i];
-                std::memcpy(&x0[i * n], (*j.x0s)[a + i].data(), sizeof(double) * n);
-                std::memcpy(&lo[i * n], p.lower().data(), sizeof(double) * n);
-                std::memcpy(&up[i * n], p.upper().data(), sizeof(double) * n);
-                if (np > 0) std::memcpy(&prm[i * np], p.params().data(), sizeof(double) * np);
+                detail::stage_copy(&x0[i * n], (*j.x0s)[a + i].data(), n);
+                detail::stage_copy(&lo[i * n], p.lower().data(), n);
+                detail::stage_copy(&up[i * n], p.upper().data(), n);
+                if (np > 0) detail::stage_copy(&prm[i * np], p.params().data(), np);
             }
+#if defined(__SSE2__)
+            _mm_sfence();
+#endif
         });
     };
     const tb_unpack_fn unpack = [](void* u, int64_t a, int64_t b, const tb_batch_result* r) {
         Job& j = *static_cast<Job*>(u);
+        if (j.prep->joinable()) j.prep->join();
+        if (*j.prep_err) return;  // rethrown after the call
         const int n = j.n;
         j.pool->run(b - a, kGrain, [&](int64_t s, int64_t e) {
             try {
                 for (int64_t i = s; i < e; ++i) {
                     SolveReport& rep = j.out->reports[a + i];
-                    rep.x_star.assign(&r->x_star[i * n], &r->x_star[i * n] + n);
+                    std::memcpy(rep.x_star.data(), &r->x_star[i * n], sizeof(double) * n);
                     rep.f_star = r->f_star[i];
                     rep.pg_norm = r->pg_norm[i];
                     rep.status = static_cast<SolveStatus>(r->status[i]);
@@ -279,6 +317,8 @@ BatchResult solve_batch(const std::vector<P>& problems, const std::vector<Vector
     tb_batch_result r{};
     const tb_tron_config c = to_c(cfg);
     const int rc = tb_solve_batch_packed(ctx.get(), P::family, n, N, &c, pack, unpack, &job, &r);
+    if (prep.joinable()) prep.join();  // an error before any unpack
+    if (prep_err) std::rethrow_exception(prep_err);
     if (job.err) std::rethrow_exception(job.err);
     if (rc == TB_E_INVALID_ARGUMENT) throw std::invalid_argument(tb_last_error());
     if (rc == TB_E_PROBLEM) {

@@ -6,6 +6,7 @@ from .tron import (  # noqa: F401
     Family,
     FactorizationError,
     KernelForm,
+    LaunchOrder,
     ImbalanceStats,
     ProblemBatch,
     SingularFactorError,

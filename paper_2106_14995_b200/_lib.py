@@ -90,6 +90,7 @@ SIGNATURES = {
     "tb_context_destroy": (C.c_int, [C.c_void_p]),
     "tb_context_set_mode": (C.c_int, [C.c_void_p, C.c_int32, C.c_int32]),
     "tb_context_set_form": (C.c_int, [C.c_void_p, C.c_int32]),
+    "tb_context_set_order": (C.c_int, [C.c_void_p, C.c_int32]),
     "tb_solve_batch": (
         C.c_int,
         [C.c_void_p, C.POINTER(ProblemBatchC), C.POINTER(TronConfigC), C.POINTER(BatchResultC)],

@@ -13,7 +13,11 @@
 #include <cstdlib>
 #include <cstring>
 #include <string>
+#include <thread>
 #include <vector>
+#if defined(__SSE2__)
+#include <emmintrin.h>
+#endif
 
 #include "../../include/tb_capi.h"
 #include "tb_families.h"
@@ -104,6 +108,8 @@ struct DevState {
     // stream waits for it, so overlapping async solves never share the
     // workspace's work counter and Hessian slices
     cudaEvent_t ws_ev = nullptr;
+    DevBuf ord;                     // launch-order workspace (tron_order.cu)
+    cudaEvent_t ord_ev = nullptr;   // its last user, like ws_ev
 };
 
 __global__ void first_error_kernel(const int32_t* status, long long count, unsigned long long* out) {
@@ -118,6 +124,7 @@ struct tb_context {
     int mode = TB_MODE_EXACT;
     int fast_forward = 1;
     int form = TB_FORM_AUTO;
+    int order = TB_ORDER_AUTO;
 };
 
 extern "C" {
@@ -186,6 +193,7 @@ int tb_context_create(const int32_t* devices, int32_t n_devices, tb_context** ou
         if (e == cudaSuccess) e = cudaEventCreateWithFlags(&d.fork, cudaEventDisableTiming);
         if (e == cudaSuccess) e = cudaEventCreateWithFlags(&d.join, cudaEventDisableTiming);
         if (e == cudaSuccess) e = cudaEventCreateWithFlags(&d.ws_ev, cudaEventDisableTiming);
+        if (e == cudaSuccess) e = cudaEventCreateWithFlags(&d.ord_ev, cudaEventDisableTiming);
         if (e != cudaSuccess) {
             ctx->devs.push_back(d);  // the partially created streams / events are released with it
             tb_context_destroy(ctx);
@@ -213,6 +221,7 @@ int tb_context_destroy(tb_context* ctx) {
         if (d.fork) cudaEventDestroy(d.fork);
         if (d.join) cudaEventDestroy(d.join);
         if (d.ws_ev) cudaEventDestroy(d.ws_ev);
+        if (d.ord_ev) cudaEventDestroy(d.ord_ev);
         if (d.stream) cudaStreamDestroy(d.stream);
         for (auto& a : d.aux)
             if (a) cudaStreamDestroy(a);
@@ -256,6 +265,14 @@ int tb_context_set_form(tb_context* ctx, int32_t form) {
     if (form != TB_FORM_AUTO && form != TB_FORM_WARP && form != TB_FORM_THREAD && form != TB_FORM_BLOCK)
         return set_err(TB_E_INVALID_ARGUMENT, "unknown kernel form %d", form);
     ctx->form = form;
+    return TB_OK;
+}
+
+int tb_context_set_order(tb_context* ctx, int32_t order) {
+    if (!ctx) return set_err(TB_E_INVALID_ARGUMENT, "null context");
+    if (order != TB_ORDER_AUTO && order != TB_ORDER_INDEX && order != TB_ORDER_START_PG)
+        return set_err(TB_E_INVALID_ARGUMENT, "unknown launch order %d", order);
+    ctx->order = order;
     return TB_OK;
 }
 
@@ -311,6 +328,61 @@ int check_batch(const tb_problem_batch* b, int64_t* nparams) {
 }
 
 constexpr int64_t kChunkMin = 4096;  // problems per chunk of the host-buffer pipeline
+
+// Copy into page-locked staging with non-temporal stores: a DMA that reads
+// lines the CPU just wrote (still dirty in its caches) runs at ~17 GB/s on
+// the B200 boxes, the same bytes written with streaming stores at the full
+// ~53 GB/s (scripts/micro/h2d_staging.cu), and the copy itself is faster.
+void stream_memcpy(void* dst, const void* src, size_t bytes) {
+#if defined(__SSE2__)
+    char* d = static_cast<char*>(dst);
+    const char* s = static_cast<const char*>(src);
+    const size_t head = std::min(bytes, (size_t)((16 - (reinterpret_cast<uintptr_t>(d) & 15)) & 15));
+    std::memcpy(d, s, head);
+    size_t i = head;
+    for (; i + 64 <= bytes; i += 64) {
+        const __m128i a = _mm_loadu_si128(reinterpret_cast<const __m128i*>(s + i));
+        const __m128i b = _mm_loadu_si128(reinterpret_cast<const __m128i*>(s + i + 16));
+        const __m128i c = _mm_loadu_si128(reinterpret_cast<const __m128i*>(s + i + 32));
+        const __m128i e = _mm_loadu_si128(reinterpret_cast<const __m128i*>(s + i + 48));
+        _mm_stream_si128(reinterpret_cast<__m128i*>(d + i), a);
+        _mm_stream_si128(reinterpret_cast<__m128i*>(d + i + 16), b);
+        _mm_stream_si128(reinterpret_cast<__m128i*>(d + i + 32), c);
+        _mm_stream_si128(reinterpret_cast<__m128i*>(d + i + 48), e);
+    }
+    _mm_sfence();
+    std::memcpy(d + i, s + i, bytes - i);
+#else
+    std::memcpy(dst, src, bytes);
+#endif
+}
+
+// Host copies between caller (pageable) memory and the pinned staging: one
+// thread moves ~17 GB/s, so copies of a few MB are split over host threads
+// (the staging of a ranked C2 batch is 28 MB in, 6 MB out); `to_staging`
+// selects the streaming stores.
+void par_memcpy(void* dst, const void* src, size_t bytes, bool to_staging = false) {
+    constexpr size_t kPiece = size_t(1) << 18;
+    const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
+    const size_t t = std::min<size_t>(std::min<size_t>(hw, 8), bytes / kPiece);
+    auto copy = [&](void* d, const void* s, size_t n) {
+        if (to_staging) stream_memcpy(d, s, n);
+        else std::memcpy(d, s, n);
+    };
+    if (t <= 1) {
+        copy(dst, src, bytes);
+        return;
+    }
+    std::vector<std::thread> th;
+    th.reserve(t - 1);
+    auto part = [&](size_t k) {
+        const size_t a = bytes * k / t, b = bytes * (k + 1) / t;
+        copy(static_cast<char*>(dst) + a, static_cast<const char*>(src) + a, b - a);
+    };
+    for (size_t k = 1; k < t; ++k) th.emplace_back(part, k);
+    part(0);
+    for (auto& x : th) x.join();
+}
 
 // page-locked (or registered) host memory: async copies from pageable memory
 // block the host, which would serialise the chunk pipeline
@@ -404,6 +476,7 @@ tbdev::KernelArgs make_args(const tb_problem_batch* b, int64_t np, const tb_tron
     a.next = nullptr;
     a.form = form;
     a.skip = nullptr;
+    a.order = nullptr;
     return a;
 }
 
@@ -423,6 +496,36 @@ cudaError_t release_ws(DevState& d, const tbdev::KernelArgs& a, cudaStream_t st)
     return a.ws ? cudaEventRecord(d.ws_ev, st) : cudaSuccess;
 }
 
+// Launch order (tron_order.cu).  AUTO ranks where the start
+// projected-gradient norm was measured to predict the long solves
+// (profiles/r02_order_ab.txt, device-resident, ms, index -> ranked): the
+// branch family beyond one wave of warps (C2 7.39 -> 5.36; branch4 thread
+// form x20,467 0.80 -> 0.74, x65,536 1.16 -> 0.90) and the d = 17..32 block
+// kernel beyond one wave (ncvx32 x8,192 10.65 -> 9.45, ncvx24 7.10 -> 6.93).
+// Elsewhere the ranking does not pay (ncvx d <= 16 and boxqp warp / thread
+// forms, the d >= 33 block kernel: 0-17 % slower), so those keep index order.
+bool want_order(int family, const tbdev::KernelArgs& a, int mode) {
+    if (mode == TB_ORDER_INDEX || a.count < 2 || a.flops) return false;  // counting runs: untimed
+    if (mode == TB_ORDER_START_PG) return true;
+    const long long wave = 32LL * tbdev::device_sm_count();
+    const int form = tbdev::tron_form(family, a);
+    if (family == TB_FAMILY_BRANCH) return form == TB_FORM_THREAD ? a.count >= 16384 : a.count > wave;
+    return form == TB_FORM_BLOCK && a.n >= 17 && a.n <= 32 && a.count > 16LL * tbdev::device_sm_count();
+}
+// rank the launch's problems into the device's order workspace on `st`
+// (ordered after the previous user of that workspace, like attach_ws)
+cudaError_t attach_order(DevState& d, int family, tbdev::KernelArgs& a, int mode, cudaStream_t st) {
+    a.order = nullptr;
+    if (!want_order(family, a, mode)) return cudaSuccess;
+    cudaError_t e = d.ord.ensure(tbdev::order_ws_bytes(a.count));
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(st, d.ord_ev, 0);
+    if (e == cudaSuccess) e = tbdev::launch_order(family, a, d.ord.p, st, &a.order);
+    return e;
+}
+cudaError_t release_order(DevState& d, const tbdev::KernelArgs& a, cudaStream_t st) {
+    return a.order ? cudaEventRecord(d.ord_ev, st) : cudaSuccess;
+}
+
 // Device-resident batch on the warp kernel: `nch` concurrent chunk launches
 // forked from `st` onto the device's chunk streams and joined back, so the
 // long-running problems of one chunk overlap the bulk of the others (the
@@ -436,6 +539,11 @@ cudaError_t launch_split(DevState& d, int family, const tbdev::KernelArgs& a, cu
         tbdev::KernelArgs c = a;
         const int n = a.n;
         c.count = a1 - a0;
+        if (c.order) {  // ranked: chunk k takes launch slots [a0, a1) of the whole batch
+            c.order += a0;
+            e = tbdev::launch_tron(family, c, d.aux[k]);
+            continue;
+        }
         c.x0 += a0 * n;
         c.lo += a0 * n;
         c.up += a0 * n;
@@ -491,7 +599,9 @@ extern "C" int tb_solve_batch_async(tb_context* ctx, const tb_problem_batch* b, 
     tbdev::KernelArgs a = make_args(b, np, cfg, ctx->fast_forward, ctx->form, b->x0, b->lower, b->upper, b->params,
                                     b->params_stride, b->count, o);
     CUDA_TRY(attach_ws(d, b->family, a, st));
-    CUDA_TRY(launch_split(d, b->family, a, st, device_chunks(a, b->family)));
+    CUDA_TRY(attach_order(d, b->family, a, ctx->order, st));
+    CUDA_TRY(launch_split(d, b->family, a, st, a.order ? 1 : device_chunks(a, b->family)));
+    CUDA_TRY(release_order(d, a, st));
     CUDA_TRY(release_ws(d, a, st));
     return TB_OK;
 }
@@ -558,6 +668,7 @@ static int solve_batch_impl(tb_context* ctx, const tb_problem_batch* b, const tb
     int64_t first_bad = -1;  // first problem the reference would have thrown on (batch.hpp:75-76)
     int bad_status = 0;
     std::vector<int> nchs(G, 1);
+    std::vector<char> rankeds(G, 0);
     for (int k = 0; k < G; ++k) {
         DevState& d = ctx->devs[k];
         CUDA_TRY(cudaSetDevice(d.device));
@@ -568,7 +679,21 @@ static int solve_batch_impl(tb_context* ctx, const tb_problem_batch* b, const tb
         const bool out_stage = out_host && !out_pinned && c > 0;
         size_t ws_need = 0;  // > 0: the persistent block kernel (one workspace per device): no chunking
         CUDA_TRY(tbdev::tron_ws_need(b->family, n, c, ctx->form, &ws_need));
-        const int nch = (staged && ws_need == 0 && c >= 2 * kChunkMin)
+        // Ranked partitions solve in ONE launch in rank order
+        // once the whole partition is on the device (a problem's rank spans
+        // the partition), so their inputs go over in one piece (pageable ones
+        // through a multi-threaded host copy into the staging); only the
+        // callers' pack callbacks keep the chunks (packing chunk i+1 overlaps
+        // chunk i's transfer)
+        bool ranked = false;
+        if (staged) {
+            tbdev::KernelArgs stub = make_args(b, np, cfg, ctx->fast_forward, ctx->form, nullptr, nullptr, nullptr,
+                                               nullptr, stride, c, OutPtrs{});
+            stub.flops = r->flops;  // a counting run is never ranked
+            stub.route_count = c;
+            ranked = want_order(b->family, stub, ctx->order);
+        }
+        const int nch = (staged && ws_need == 0 && c >= 2 * kChunkMin && (!ranked || cb))
                             ? (int)std::min<int64_t>(max_chunks(true), c / kChunkMin)
                             : 1;
         nchs[k] = nch;
@@ -607,6 +732,25 @@ static int solve_batch_impl(tb_context* ctx, const tb_problem_batch* b, const tb
                 ofull.status = carve(d.out.p, c, n).status;
             }
         }
+        // the whole partition's launch arguments (device copies of the inputs)
+        auto part_args = [&]() {
+            const double *x0, *lw, *up, *prm;
+            if (in_host) {
+                x0 = reinterpret_cast<const double*>(inp);
+                lw = reinterpret_cast<const double*>(inp + vb);
+                up = reinterpret_cast<const double*>(inp + 2 * vb);
+                prm = pb ? reinterpret_cast<const double*>(inp + 3 * vb) : nullptr;
+            } else {
+                x0 = b->x0 + lo[k] * n;
+                lw = b->lower + lo[k] * n;
+                up = b->upper + lo[k] * n;
+                prm = np > 0 ? b->params + lo[k] * stride : nullptr;
+            }
+            tbdev::KernelArgs a = make_args(b, np, cfg, ctx->fast_forward, ctx->form, x0, lw, up, prm, stride, c, ofull);
+            a.route_count = c;
+            return a;
+        };
+        rankeds[k] = ranked;
         for (int ch = 0; ch < nch; ++ch) {
             cudaStream_t st = nch > 1 ? d.aux[ch] : d.stream;
             const int64_t a0 = c * ch / nch, a1 = c * (ch + 1) / nch, cc = a1 - a0;  // local range
@@ -629,10 +773,10 @@ static int solve_batch_impl(tb_context* ctx, const tb_problem_batch* b, const tb
                         cb->pack(cb->user, g0, g0 + cc, reinterpret_cast<double*>(hx), reinterpret_cast<double*>(hl),
                                  reinterpret_cast<double*>(hu), cpb ? reinterpret_cast<double*>(hp) : nullptr);
                     } else {
-                        std::memcpy(hx, x0, cvb);
-                        std::memcpy(hl, lw, cvb);
-                        std::memcpy(hu, up, cvb);
-                        if (cpb) std::memcpy(hp, prm, cpb);
+                        par_memcpy(hx, x0, cvb, true);
+                        par_memcpy(hl, lw, cvb, true);
+                        par_memcpy(hu, up, cvb, true);
+                        if (cpb) par_memcpy(hp, prm, cpb, true);
                     }
                     x0 = reinterpret_cast<const double*>(hx);
                     lw = reinterpret_cast<const double*>(hl);
@@ -648,6 +792,7 @@ static int solve_batch_impl(tb_context* ctx, const tb_problem_batch* b, const tb
                 up = reinterpret_cast<const double*>(du);
                 prm = cpb ? reinterpret_cast<const double*>(dp) : nullptr;
             }
+            if (ranked) continue;  // inputs only; the ranked launch follows the loop
             auto off = [&](auto* p, int64_t m) { return p ? p + a0 * m : p; };
             OutPtrs o{off(ofull.x_star, n), off(ofull.f_star, 1), off(ofull.pg, 1), off(ofull.status, 1),
                       off(ofull.iters, 1), off(ofull.cg, 1),    off(ofull.fev, 1), off(ofull.flops, 1),
@@ -656,8 +801,15 @@ static int solve_batch_impl(tb_context* ctx, const tb_problem_batch* b, const tb
             a.route_count = c;  // kernel-form routing by the partition, not the pipeline chunk
             CUDA_TRY(attach_ws(d, b->family, a, st));
             if (ch == 0) CUDA_TRY(cudaEventRecord(d.ev[1], st));
-            if (!staged) CUDA_TRY(launch_split(d, b->family, a, st, device_chunks(a, b->family)));
-            else CUDA_TRY(tbdev::launch_tron(b->family, a, st));
+            if (!staged) {
+                CUDA_TRY(attach_order(d, b->family, a, ctx->order, st));
+                // ranked: one launch in rank order (concurrent chunk launches
+                // would interleave their dispatch and blur the order)
+                CUDA_TRY(launch_split(d, b->family, a, st, a.order ? 1 : device_chunks(a, b->family)));
+                CUDA_TRY(release_order(d, a, st));
+            } else {
+                CUDA_TRY(tbdev::launch_tron(b->family, a, st));
+            }
             CUDA_TRY(release_ws(d, a, st));
             if (ch == nch - 1 && nch == 1) CUDA_TRY(cudaEventRecord(d.ev[2], st));
             if (out_host && cc > 0) {
@@ -687,7 +839,37 @@ static int solve_batch_impl(tb_context* ctx, const tb_problem_batch* b, const tb
                 CUDA_TRY(cudaEventRecord(d.join, d.aux[ch]));
                 CUDA_TRY(cudaStreamWaitEvent(d.stream, d.join, 0));
             }
-            CUDA_TRY(cudaEventRecord(d.ev[2], d.stream));  // chunked: includes the last D2H
+            if (!ranked) CUDA_TRY(cudaEventRecord(d.ev[2], d.stream));  // chunked: includes the last D2H
+        }
+        if (ranked) {
+            tbdev::KernelArgs a = part_args();
+            CUDA_TRY(attach_ws(d, b->family, a, d.stream));
+            CUDA_TRY(cudaEventRecord(d.ev[1], d.stream));
+            CUDA_TRY(attach_order(d, b->family, a, ctx->order, d.stream));
+            CUDA_TRY(tbdev::launch_tron(b->family, a, d.stream));
+            CUDA_TRY(release_order(d, a, d.stream));
+            CUDA_TRY(release_ws(d, a, d.stream));
+            CUDA_TRY(cudaEventRecord(d.ev[2], d.stream));
+            if (out_host) {
+                auto tgt = [&](auto* user, auto* stage, int64_t m) -> decltype(user) {
+                    if (!user && !(cb && stage)) return nullptr;  // callbacks: every report field
+                    return out_stage ? stage : user + lo[k] * m;
+                };
+                auto cp = [&](void* dst, const void* src, size_t bytes) -> cudaError_t {
+                    if (!dst || !src) return cudaSuccess;
+                    return cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, d.stream);
+                };
+                const OutPtrs& o = ofull;
+                CUDA_TRY(cp(tgt(r->x_star, hst.x_star, n), o.x_star, sizeof(double) * c * n));
+                CUDA_TRY(cp(tgt(r->f_star, hst.f_star, 1), o.f_star, sizeof(double) * c));
+                CUDA_TRY(cp(tgt(r->pg_norm, hst.pg, 1), o.pg, sizeof(double) * c));
+                CUDA_TRY(cp(tgt(r->status, hst.status, 1), o.status, sizeof(int32_t) * c));
+                CUDA_TRY(cp(tgt(r->iterations, hst.iters, 1), o.iters, sizeof(int32_t) * c));
+                CUDA_TRY(cp(tgt(r->cg_iterations, hst.cg, 1), o.cg, sizeof(int64_t) * c));
+                CUDA_TRY(cp(tgt(r->f_evals, hst.fev, 1), o.fev, sizeof(int64_t) * c));
+                CUDA_TRY(cp(tgt(r->flops, hst.flops, 1), o.flops, sizeof(int64_t) * c));
+                CUDA_TRY(cp(tgt(r->wall_time, hst.wall, 1), o.wall, sizeof(double) * c));
+            }
         }
         CUDA_TRY(cudaEventRecord(d.ev[3], d.stream));
     }
@@ -703,7 +885,8 @@ static int solve_batch_impl(tb_context* ctx, const tb_problem_batch* b, const tb
             const OutPtrs hst = carve(d.hout.p, c, n);
             const int nch = nchs[k];
             for (int ch = 0; ch < nch; ++ch) {
-                CUDA_TRY(cudaStreamSynchronize(nch > 1 ? d.aux[ch] : d.stream));
+                // ranked: every result arrives with the partition's one D2H
+                CUDA_TRY(cudaStreamSynchronize(nch > 1 && !rankeds[k] ? d.aux[ch] : d.stream));
                 const int64_t a0 = c * ch / nch, a1 = c * (ch + 1) / nch, cc = a1 - a0, g0 = lo[k] + a0;
                 if (cb) {  // the chunk's reports, straight from the staging
                     for (int64_t i = 0; i < cc && first_bad < 0; ++i)
@@ -725,7 +908,7 @@ static int solve_batch_impl(tb_context* ctx, const tb_problem_batch* b, const tb
                     continue;
                 }
                 auto out = [&](auto* user, auto* stage, int64_t m) {
-                    if (user) std::memcpy(user + g0 * m, stage + a0 * m, sizeof(*user) * (size_t)(cc * m));
+                    if (user) par_memcpy(user + g0 * m, stage + a0 * m, sizeof(*user) * (size_t)(cc * m));
                 };
                 out(r->x_star, hst.x_star, n);
                 out(r->f_star, hst.f_star, 1);

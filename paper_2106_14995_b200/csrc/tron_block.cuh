@@ -1122,7 +1122,7 @@ __device__ __forceinline__ double* blk_lglob(const KernelArgs& a, bool asmem) {
     return base + (size_t)blockIdx.x * (D * (D + 1) / 2);
 }
 
-template <int FAM, int D, bool ASMEM, bool COUNT>
+template <int FAM, int D, bool ASMEM, bool COUNT, bool ORD = false>
 __global__ void __launch_bounds__(D, BlkMinBlocks<D>::value) tron_block_kernel(const __grid_constant__ KernelArgs a) {
     extern __shared__ double smem[];
     using SL = BlkLayout<D, ASMEM>;
@@ -1161,9 +1161,10 @@ __global__ void __launch_bounds__(D, BlkMinBlocks<D>::value) tron_block_kernel(c
     for (;;) {
         if (t == 0) *pid_slot = atomicAdd(work, 1u);
         __syncthreads();
-        const long long pid = *pid_slot;
+        const long long k = *pid_slot;
         __syncthreads();
-        if (pid >= a.count) break;
+        if (k >= a.count) break;
+        const long long pid = ORD ? (long long)a.order[k] : k;  // ORD: ranked work items (tron_order.cu)
         W.memo_clear();  // a new problem: no memoised factor (ordered by the barriers before ccf)
         const unsigned long long t_start = globaltimer();
         W.fl = 0;

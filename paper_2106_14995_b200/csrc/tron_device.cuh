@@ -127,7 +127,12 @@ struct KernelArgs {
     // device flag: when non-null and set, the launch does nothing (ADMM
     // iterations enqueued past convergence, tb_admm_run)
     const int* skip;
+    // launch order (tron_order.cu): the k-th block / thread / work item
+    // solves problem order[k]; null = index order
+    const uint32_t* order;
 };
+
+
 
 // shared memory per warp (doubles; every region starts at an even offset)
 template <int D>
@@ -1221,12 +1226,14 @@ __device__ __forceinline__ void tron_solve_one(const KernelArgs& a, const long l
 constexpr int kLatencyBlocks = 16;
 
 // One problem per warp (one warp per block); MINB resident blocks per SM.
-template <int FAM, int D, bool COUNT, int MINB = WarpMinBlocks<D>::value>
+// ORD: launch slot k solves problem a.order[k] (tron_order.cu; a separate
+// instantiation, so index-order launches keep their code unchanged).
+template <int FAM, int D, bool COUNT, int MINB = WarpMinBlocks<D>::value, bool ORD = false>
 __global__ void __launch_bounds__(32, MINB) tron_solve_kernel(const __grid_constant__ KernelArgs a) {
     extern __shared__ double smem[];
     const long long pid = blockIdx.x;
     if (pid >= a.count || (a.skip && *a.skip)) return;
-    tron_solve_one<FAM, D, COUNT>(a, pid, smem);
+    tron_solve_one<FAM, D, COUNT>(a, ORD ? (long long)a.order[pid] : pid, smem);
 }
 
 }  // namespace tbdev

@@ -70,6 +70,7 @@ cudaError_t counter_slot(unsigned long long** out) {
 }
 
 int tron_form(int family, const KernelArgs& a) { return resolve_form(family, a); }
+int device_sm_count() { return device_sms(); }
 
 int max_warp_dim() { return 32; }
 int max_dim() { return 128; }

@@ -37,6 +37,9 @@ static cudaError_t launch_fdc(const KernelArgs& a, cudaStream_t st) {
         const long long total = a.route_count > a.count ? a.route_count : a.count;
         if (total <= (long long)kLatencyBlocks * device_sms()) kern = tron_solve_kernel<FAM, D, false, kLatencyBlocks>;
     }
+    // ranked launch (tron_order.cu; never a counting run)
+    if constexpr (!COUNT)
+        if (a.order) kern = tron_solve_kernel<FAM, D, false, WarpMinBlocks<D>::value, true>;
     if (smem > 48 * 1024) {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return e;
@@ -75,11 +78,11 @@ inline bool use_block(int n, int form) {
 inline int block_dim(int n) { return n <= 32 ? 32 : (n <= 64 ? 64 : 128); }
 
 // persistent grid: resident blocks per SM x SMs, capped by the batch
-template <int FAM, int D, bool ASMEM, bool COUNT>
+template <int FAM, int D, bool ASMEM, bool COUNT, bool ORD = false>
 static cudaError_t blk_grid(long long count, long long* grid, size_t* smem_out) {
     using SL = BlkLayout<D, ASMEM>;
     const size_t smem = sizeof(double) * (size_t)SL::total();
-    auto kern = tron_block_kernel<FAM, D, ASMEM, COUNT>;
+    auto kern = tron_block_kernel<FAM, D, ASMEM, COUNT, ORD>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     int dev = 0, sms = 0, per_sm = 0;
@@ -92,18 +95,20 @@ static cudaError_t blk_grid(long long count, long long* grid, size_t* smem_out) 
     return cudaSuccess;
 }
 
-template <int FAM, int D, bool ASMEM, bool COUNT>
+template <int FAM, int D, bool ASMEM, bool COUNT, bool ORD = false>
 static cudaError_t launch_blk_c(const KernelArgs& a, cudaStream_t st) {
+    if constexpr (!COUNT && !ORD)
+        if (a.order) return launch_blk_c<FAM, D, ASMEM, false, true>(a, st);  // ranked work items
     long long grid = 0;
     size_t smem = 0;
-    cudaError_t e = blk_grid<FAM, D, ASMEM, COUNT>(a.count, &grid, &smem);
+    cudaError_t e = blk_grid<FAM, D, ASMEM, COUNT, ORD>(a.count, &grid, &smem);
     if (e != cudaSuccess) return e;
     using SL = BlkLayout<D, ASMEM>;
     const size_t need = kBlkWsHeader + (ASMEM ? 0 : sizeof(double) * (size_t)grid * D * D) +
                         (SL::LP < SL::LPFULL ? sizeof(double) * (size_t)grid * SL::LPFULL : 0);
     if (!a.ws || a.ws_bytes < need) return cudaErrorMemoryAllocation;
     if ((e = cudaMemsetAsync(a.ws, 0, sizeof(unsigned), st)) != cudaSuccess) return e;
-    tron_block_kernel<FAM, D, ASMEM, COUNT><<<(unsigned)grid, D, smem, st>>>(a);
+    tron_block_kernel<FAM, D, ASMEM, COUNT, ORD><<<(unsigned)grid, D, smem, st>>>(a);
     note_launches(1);
     return cudaGetLastError();
 }
@@ -125,6 +130,8 @@ static cudaError_t ws_need_blk(long long count, size_t* bytes) {
     if (e != cudaSuccess) return e;
     long long g2 = 0;
     if ((e = blk_grid<FAM, D, as, true>(count, &g2, &smem)) != cudaSuccess) return e;
+    if (g2 > grid) grid = g2;
+    if ((e = blk_grid<FAM, D, as, false, true>(count, &g2, &smem)) != cudaSuccess) return e;  // ranked variant
     if (g2 > grid) grid = g2;
     using SL = BlkLayout<D, false>;
     if (!as) *bytes += sizeof(double) * (size_t)grid * D * D;

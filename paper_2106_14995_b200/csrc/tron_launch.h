@@ -19,4 +19,9 @@ void note_launches(long long k);
 // (round-robin over a pool; the launcher zeroes it on its stream)
 cudaError_t counter_slot(unsigned long long** out);
 long long launches();
+// longest-expected-first launch order (tron_order.cu) into `ws`
+// (order_ws_bytes(a.count) bytes); *order_out points into ws
+size_t order_ws_bytes(long long count);
+int device_sm_count();
+cudaError_t launch_order(int family, const KernelArgs& a, void* ws, cudaStream_t st, const uint32_t** order_out);
 }  // namespace tbdev

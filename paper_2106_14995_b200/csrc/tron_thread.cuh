@@ -685,16 +685,18 @@ __device__ __forceinline__ void tron_solve_thread(const KernelArgs& a, const lon
 // 3.09, x20,467 0.81 vs 1.28, x4,096 0.43 vs 0.57.  At n = 6 / 8 the 255-register thread form loses (7.7 vs 7.4 ms
 // branch6, 13.3 vs 3.6 ms ncvx8).  KernelForm.WARP forces the warp form.  Flop
 // counting stays in the warp kernel.
-template <int D, int FAM = TB_FAMILY_BRANCH>
+template <int D, int FAM = TB_FAMILY_BRANCH, bool ORD = false>
 __global__ void __launch_bounds__(64) tron_thread_kernel(const __grid_constant__ KernelArgs a) {
     const long long pid = blockIdx.x * (long long)blockDim.x + threadIdx.x;
     if (pid >= a.count || (a.skip && *a.skip)) return;
-    tron_solve_thread<D, FAM>(a, pid);
+    tron_solve_thread<D, FAM>(a, ORD ? (long long)a.order[pid] : pid);  // ORD: ranked launch (tron_order.cu)
 }
 
 template <int D, int FAM>
 inline cudaError_t launch_thread(const KernelArgs& a, cudaStream_t st) {
-    tron_thread_kernel<D, FAM><<<(unsigned)((a.count + 63) / 64), 64, 0, st>>>(a);
+    const unsigned grid = (unsigned)((a.count + 63) / 64);
+    if (a.order) tron_thread_kernel<D, FAM, true><<<grid, 64, 0, st>>>(a);
+    else tron_thread_kernel<D, FAM><<<grid, 64, 0, st>>>(a);
     note_launches(1);
     return cudaGetLastError();
 }

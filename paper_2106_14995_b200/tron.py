@@ -73,6 +73,17 @@ class KernelForm(enum.IntEnum):
     BLOCK = 4   # 32 / 64 / 128 threads per problem, persistent (d >= 9)
 
 
+class LaunchOrder(enum.IntEnum):
+    """tb_capi.h TB_ORDER_*: which problems of a batch start first.  Results
+    never depend on it; START_PG launches the problems in descending
+    projected-gradient norm at their clipped start points (long solves
+    first), AUTO where that was measured to pay, INDEX never."""
+
+    AUTO = 0
+    INDEX = 1
+    START_PG = 2
+
+
 @dataclass
 class TronConfig:
     """tron.hpp:54-81, same defaults."""
@@ -195,7 +206,7 @@ class Solver:
     role of solve_batch's `workers`: contiguous even partitions per device."""
 
     def __init__(self, devices: Sequence[int] = (0,), fast_forward=True,
-                 form: "KernelForm" = KernelForm.AUTO):
+                 form: "KernelForm" = KernelForm.AUTO, order: "LaunchOrder" = LaunchOrder.AUTO):
         self._lib = L.load()
         arr = (C.c_int32 * len(devices))(*devices)
         ctx = C.c_void_p()
@@ -207,6 +218,16 @@ class Solver:
         if self._lib.tb_context_set_mode(self._ctx, 0, ff) != L.TB_OK:
             raise SolverError(L.last_error())
         self.set_form(form)
+        self.set_order(order)
+
+    def set_order(self, order: "LaunchOrder") -> None:
+        """Launch order of later solves (TB_ORDER_*; results are identical)."""
+        if int(order) == 0 and not hasattr(self._lib, "tb_context_set_order"):
+            self.order = LaunchOrder.AUTO  # older library build (A/B experiments)
+            return
+        if self._lib.tb_context_set_order(self._ctx, int(order)) != L.TB_OK:
+            raise ValueError(L.last_error())
+        self.order = LaunchOrder(int(order))
 
     def set_form(self, form: "KernelForm") -> None:
         """Kernel form of later solves (TB_FORM_*; results are identical)."""

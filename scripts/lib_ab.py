@@ -1,5 +1,6 @@
 """A/B of library builds on the same device-resident batches (interleaved
-rounds, median kernel time): python scripts/lib_ab.py fam:n[,fam:n] lib1.so lib2.so ..."""
+rounds, median kernel time): python scripts/lib_ab.py fam:n[,fam:n] lib1.so lib2.so ...
+(AB_ORDER=INDEX|START_PG|AUTO sets the launch order where the build has it)"""
 import os
 import subprocess
 import sys
@@ -14,6 +15,9 @@ from paper_2106_14995_b200 import ProblemBatch, Solver, synth
 dev = torch.device('cuda', 0)
 t = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(dev)
 s = Solver((0,))
+if os.environ.get("AB_ORDER") and hasattr(s._lib, "tb_context_set_order"):
+    from paper_2106_14995_b200 import LaunchOrder
+    s.set_order(LaunchOrder[os.environ["AB_ORDER"]])
 for w in os.environ['AB_WORK'].split(','):
     fam, n = w.split(':'); n = int(n)
     name = fam.rstrip('0123456789'); dim = int(fam[len(name):])
