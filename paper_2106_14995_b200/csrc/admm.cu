@@ -44,9 +44,21 @@ __global__ void admm_gen_kernel(tb_admm_view v, const int* stop) {
 // one branch TRON solve per thread (tron_thread.cuh; in place: each thread
 // reads its x0 before it writes x*).  The stages touch disjoint state.
 constexpr int kThreadBlock = 64;
+// The thread-form branch stage is ranked by start projected gradient
+// (tron_order.cu) when the shard needs more than one wave of
+// it (4 blocks of 64 threads per SM): the long branches then start in the
+// first wave.  profiles/r02_ab_admm_order.txt: C5 (70,000 branches, ~1.9
+// waves) 1.977 -> 1.877 ms per iteration; C4 (20,467, one wave) would lose
+// 4 % (1.391 -> 1.445: every branch starts at once anyway), so it is not
+// ranked.  0 disables.
+#ifndef TB_ADMM_ORDER
+#define TB_ADMM_ORDER 1
+#endif
+bool admm_ranked(long long cnt) { return TB_ADMM_ORDER && cnt > 4LL * kThreadBlock * tbdev::device_sm_count(); }
 #ifndef TB_ADMM_BRANCH_MINB
 #define TB_ADMM_BRANCH_MINB 1  // resident 64-thread blocks per SM the register budget must allow
 #endif
+template <bool ORD>
 __global__ void __launch_bounds__(kThreadBlock, TB_ADMM_BRANCH_MINB)
     admm_gen_branch_kernel(const __grid_constant__ tbdev::KernelArgs k, tb_admm_view v, int gen_blocks) {
     if (stopped(k.skip)) return;
@@ -56,7 +68,7 @@ __global__ void __launch_bounds__(kThreadBlock, TB_ADMM_BRANCH_MINB)
         return;
     }
     const long long pid = (long long)(blockIdx.x - gen_blocks) * kThreadBlock + threadIdx.x;
-    if (pid < k.count) tbdev::tron_solve_thread<4, TB_FAMILY_BRANCH>(k, pid);
+    if (pid < k.count) tbdev::tron_solve_thread<4, TB_FAMILY_BRANCH>(k, ORD ? (long long)k.order[pid] : pid);
 }
 
 // first branch of [0, n) whose solve ended where the reference throws
@@ -366,6 +378,7 @@ struct tb_admm {
     double* eta = nullptr;
     int* round_max = nullptr;          // device: largest per-branch round count of this iteration
     long long* rounds_total = nullptr;  // device: sum over iterations
+    void* ord = nullptr;                // launch-order workspace of the branch stage (tron_order.cu)
 };
 
 namespace {
@@ -515,6 +528,7 @@ int tb_admm_create(const tb_admm_grid* gr, const tb_admm_options* opt, int32_t d
         a->upper = dalloc<double>(a, (size_t)nl * D, &err);
         if (err == cudaSuccess) err = upload<double>(a->upper, hs.br_upper, (size_t)nl * D);
         a->status = dalloc<int32_t>(a, (size_t)nl, &err);
+        if (D == 4 && admm_ranked(nl)) a->ord = dalloc<char>(a, tbdev::order_ws_bytes(nl), &err);
         a->res = dalloc<unsigned long long>(a, 3, &err);
         a->cost = dalloc<double>(a, 1, &err);
         a->stop = dalloc<int>(a, 2, &err);
@@ -620,8 +634,13 @@ int enqueue_components(tb_admm* a, cudaStream_t st, const int* stop) {
         k.up = a->upper + a->br_lo * 4;
         k.x_star = a->x + a->br_lo * 4;  // in place: each thread reads its x0 first
         const long long blocks = gen_blocks + (cnt + kThreadBlock - 1) / kThreadBlock;
+        if (a->ord && admm_ranked(cnt)) {
+            const cudaError_t e = tbdev::launch_order(TB_FAMILY_BRANCH, k, a->ord, st, &k.order);
+            if (e != cudaSuccess) return fail(TB_E_CUDA, cudaGetErrorString(e));
+        }
         if (blocks > 0) {
-            admm_gen_branch_kernel<<<(unsigned)blocks, kThreadBlock, 0, st>>>(k, a->v, gen_blocks);
+            if (k.order) admm_gen_branch_kernel<true><<<(unsigned)blocks, kThreadBlock, 0, st>>>(k, a->v, gen_blocks);
+            else admm_gen_branch_kernel<false><<<(unsigned)blocks, kThreadBlock, 0, st>>>(k, a->v, gen_blocks);
             tbdev::note_launches(1);
         }
     } else {
