@@ -74,6 +74,9 @@ extern "C" {
 #define TB_ORDER_AUTO 0
 #define TB_ORDER_INDEX 1
 #define TB_ORDER_START_PG 2
+/* the caller's own order (a batch it sorted by its own cost estimate), as
+ * ONE launch: problem k starts k-th */
+#define TB_ORDER_CALLER 3
 
 /* TronConfig (tron.hpp:54-81), field for field; std::optional delta0 becomes
  * has_delta0 + delta0. */

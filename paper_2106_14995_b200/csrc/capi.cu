@@ -270,7 +270,7 @@ int tb_context_set_form(tb_context* ctx, int32_t form) {
 
 int tb_context_set_order(tb_context* ctx, int32_t order) {
     if (!ctx) return set_err(TB_E_INVALID_ARGUMENT, "null context");
-    if (order != TB_ORDER_AUTO && order != TB_ORDER_INDEX && order != TB_ORDER_START_PG)
+    if (order != TB_ORDER_AUTO && order != TB_ORDER_INDEX && order != TB_ORDER_START_PG && order != TB_ORDER_CALLER)
         return set_err(TB_E_INVALID_ARGUMENT, "unknown launch order %d", order);
     ctx->order = order;
     return TB_OK;
@@ -522,6 +522,9 @@ cudaError_t attach_order(DevState& d, int family, tbdev::KernelArgs& a, int mode
     if (e == cudaSuccess) e = tbdev::launch_order(family, a, d.ord.p, st, &a.order);
     return e;
 }
+// ranked launches, and TB_ORDER_CALLER (the caller sorted the batch), run as
+// one launch in order
+bool one_launch(const tbdev::KernelArgs& a, int mode) { return a.order || mode == TB_ORDER_CALLER; }
 cudaError_t release_order(DevState& d, const tbdev::KernelArgs& a, cudaStream_t st) {
     return a.order ? cudaEventRecord(d.ord_ev, st) : cudaSuccess;
 }
@@ -600,7 +603,7 @@ extern "C" int tb_solve_batch_async(tb_context* ctx, const tb_problem_batch* b, 
                                     b->params_stride, b->count, o);
     CUDA_TRY(attach_ws(d, b->family, a, st));
     CUDA_TRY(attach_order(d, b->family, a, ctx->order, st));
-    CUDA_TRY(launch_split(d, b->family, a, st, a.order ? 1 : device_chunks(a, b->family)));
+    CUDA_TRY(launch_split(d, b->family, a, st, one_launch(a, ctx->order) ? 1 : device_chunks(a, b->family)));
     CUDA_TRY(release_order(d, a, st));
     CUDA_TRY(release_ws(d, a, st));
     return TB_OK;
@@ -691,7 +694,7 @@ static int solve_batch_impl(tb_context* ctx, const tb_problem_batch* b, const tb
                                                nullptr, stride, c, OutPtrs{});
             stub.flops = r->flops;  // a counting run is never ranked
             stub.route_count = c;
-            ranked = want_order(b->family, stub, ctx->order);
+            ranked = want_order(b->family, stub, ctx->order) || ctx->order == TB_ORDER_CALLER;
         }
         const int nch = (staged && ws_need == 0 && c >= 2 * kChunkMin && (!ranked || cb))
                             ? (int)std::min<int64_t>(max_chunks(true), c / kChunkMin)
@@ -805,7 +808,7 @@ static int solve_batch_impl(tb_context* ctx, const tb_problem_batch* b, const tb
                 CUDA_TRY(attach_order(d, b->family, a, ctx->order, st));
                 // ranked: one launch in rank order (concurrent chunk launches
                 // would interleave their dispatch and blur the order)
-                CUDA_TRY(launch_split(d, b->family, a, st, a.order ? 1 : device_chunks(a, b->family)));
+                CUDA_TRY(launch_split(d, b->family, a, st, one_launch(a, ctx->order) ? 1 : device_chunks(a, b->family)));
                 CUDA_TRY(release_order(d, a, st));
             } else {
                 CUDA_TRY(tbdev::launch_tron(b->family, a, st));

@@ -26,6 +26,10 @@ inline int device_sms() {
     return sms[dev];
 }
 
+#ifndef TB_ORD_MINB
+#define TB_ORD_MINB 0  // experiments: resident blocks per SM of the ranked warp kernel (0: WarpMinBlocks<D>)
+#endif
+
 template <int FAM, int D, bool COUNT>
 static cudaError_t launch_fdc(const KernelArgs& a, cudaStream_t st) {
     const int np = (a.nparams + 1) & ~1;
@@ -39,7 +43,7 @@ static cudaError_t launch_fdc(const KernelArgs& a, cudaStream_t st) {
     }
     // ranked launch (tron_order.cu; never a counting run)
     if constexpr (!COUNT)
-        if (a.order) kern = tron_solve_kernel<FAM, D, false, WarpMinBlocks<D>::value, true>;
+        if (a.order) kern = tron_solve_kernel<FAM, D, false, TB_ORD_MINB ? TB_ORD_MINB : WarpMinBlocks<D>::value, true>;
     if (smem > 48 * 1024) {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return e;

@@ -82,6 +82,7 @@ class LaunchOrder(enum.IntEnum):
     AUTO = 0
     INDEX = 1
     START_PG = 2
+    CALLER = 3  # the caller sorted the batch (its own cost model): one launch in index order
 
 
 @dataclass

@@ -35,7 +35,7 @@ def test_orders_bitwise_device_resident(fam, d, N, form):
     b = synth.make(fam, N, d, seed=11 + d)
     ref = po.solve_batch(b, impl="oracle", workers=W)
     db = _dev(b)
-    for order in (LaunchOrder.START_PG, LaunchOrder.INDEX, LaunchOrder.AUTO):
+    for order in (LaunchOrder.START_PG, LaunchOrder.INDEX, LaunchOrder.AUTO, LaunchOrder.CALLER):
         s = Solver((0,), form=form, order=order)
         try:
             out = Solver.alloc_result(N, d, device=True)
@@ -81,6 +81,17 @@ def test_start_pg_order_two_partitions_and_async_streams():
         torch.cuda.synchronize()
         for k, o in enumerate(outs):
             assert_bitwise(o, ref, label=f"ranked async {k}")
+    finally:
+        s.close()
+
+
+def test_caller_order_host_buffers():
+    """TB_ORDER_CALLER: the caller's own order as one launch (host buffers go
+    over whole, like a ranked batch)."""
+    b = synth.branch(20000, 6, seed=9)
+    s = Solver((0,), order=LaunchOrder.CALLER)
+    try:
+        assert_bitwise(s.solve_batch(b), po.solve_batch(b, impl="oracle", workers=W), label="caller order")
     finally:
         s.close()
 
