@@ -1,6 +1,6 @@
 """Randomized bitwise parity fuzz (GPU vs the CPU oracle): families, dims
 1..128, TronConfig variants, bound patterns (infinite, l == u, starts outside
-the box).  python scripts/fuzz_parity.py [seconds] [seed]"""
+the box), kernel forms and launch orders.  python scripts/fuzz_parity.py [seconds] [seed]"""
 import os
 import sys
 import time
@@ -9,7 +9,7 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np  # noqa: E402
 
 from oracle import pyoracle as po  # noqa: E402
-from paper_2106_14995_b200 import KernelForm, ProblemBatch, Solver, TronConfig, synth  # noqa: E402
+from paper_2106_14995_b200 import KernelForm, LaunchOrder, ProblemBatch, Solver, TronConfig, synth  # noqa: E402
 
 FIELDS = ("x_star", "f_star", "pg_norm", "status", "iterations", "cg_iterations", "f_evals")
 budget = float(sys.argv[1]) if len(sys.argv) > 1 else 300.0
@@ -62,6 +62,8 @@ while time.time() < t_end:
         + ([KernelForm.BLOCK] if d >= 9 and fam != "branch" else [])
     form = forms[int(rng.integers(0, len(forms)))]
     s.set_form(form)
+    order = list(LaunchOrder)[int(rng.integers(0, len(LaunchOrder)))]  # START_PG ranks at any size
+    s.set_order(order)
     try:
         counted = bool(rng.random() < 0.2) and form != KernelForm.THREAD  # the thread form does not count
         res = s.solve_batch(b, x0, cfg=cfg, count_flops=counted)
@@ -76,7 +78,7 @@ while time.time() < t_end:
     else:
         if counted and not np.array_equal(np.asarray(res.flops), ref.flops):
             ok = False
-            print(f"MISMATCH {fam} d={d} n={n} seed={seed} cfg={kw} form={form.name} field flops", flush=True)
+            print(f"MISMATCH {fam} d={d} n={n} seed={seed} cfg={kw} form={form.name} order={order.name} field flops", flush=True)
         for k in FIELDS:
             a, c = np.asarray(getattr(res, k)), getattr(ref, k)
             if a.dtype.kind == "f":
@@ -85,7 +87,7 @@ while time.time() < t_end:
                 eq = a == c
             if not eq.all():
                 ok = False
-                print(f"MISMATCH {fam} d={d} n={n} seed={seed} cfg={kw} form={form.name} field {k}", flush=True)
+                print(f"MISMATCH {fam} d={d} n={n} seed={seed} cfg={kw} form={form.name} order={order.name} field {k}", flush=True)
                 break
     if not ok:
         fails += 1
