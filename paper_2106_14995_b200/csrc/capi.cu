@@ -505,7 +505,8 @@ cudaError_t release_ws(DevState& d, const tbdev::KernelArgs& a, cudaStream_t st)
 // Elsewhere the ranking does not pay (ncvx d <= 16 and boxqp warp / thread
 // forms, the d >= 33 block kernel: 0-17 % slower), so those keep index order.
 bool want_order(int family, const tbdev::KernelArgs& a, int mode) {
-    if (mode == TB_ORDER_INDEX || a.count < 2 || a.flops) return false;  // counting runs: untimed
+    // counting runs are untimed; the order is 32-bit
+    if (mode == TB_ORDER_INDEX || a.count < 2 || a.flops || a.count > 0x7fffffffLL) return false;
     if (mode == TB_ORDER_START_PG) return true;
     const long long wave = 32LL * tbdev::device_sm_count();
     const int form = tbdev::tron_form(family, a);
