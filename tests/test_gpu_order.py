@@ -96,6 +96,40 @@ def test_caller_order_host_buffers():
         s.close()
 
 
+@pytest.mark.parametrize("n", [1, 2, 3, 31, 33, 257])
+def test_start_pg_order_small_and_odd_sizes(n):
+    b = synth.branch(n, 6, seed=n)
+    ref = po.solve_batch(b, impl="oracle", workers=W)
+    s = Solver((0,), order=LaunchOrder.START_PG)
+    try:
+        assert_bitwise(s.solve_batch(b), ref, label=f"ranked host n={n}")
+        assert_bitwise(s.solve_batch(_dev(b)), ref, label=f"ranked device n={n}")
+    finally:
+        s.close()
+
+
+def test_ranked_batch_reports_the_first_failure_in_input_order():
+    """batch.hpp:75-76 in a ranked launch: the error names the first failing
+    problem in INPUT order, whatever order the problems were solved in."""
+    b = synth.branch(30000, 6, seed=12)
+    lo = np.array(b.lower, copy=True)
+    for i in (29000, 17, 5000):
+        lo[i, 1] = b.upper[i, 1] + 0.5
+    b = ProblemBatch(b.family, 6, lo, b.upper, b.params, b.x0)
+    ref = po.solve_batch(b, impl="oracle", workers=W)
+    for order in (LaunchOrder.START_PG, LaunchOrder.AUTO):
+        s = Solver((0,), order=order)
+        try:
+            with pytest.raises(Exception, match="problem 17"):
+                s.solve_batch(b)
+            out = Solver.alloc_result(b.count, 6, device=True)
+            with pytest.raises(Exception, match="problem 17"):
+                s.solve_batch(_dev(b), out=out)
+            assert np.array_equal(host(out.status), ref.status)
+        finally:
+            s.close()
+
+
 def test_set_order_rejects_unknown():
     s = Solver((0,))
     try:
