@@ -379,7 +379,12 @@ void par_memcpy(void* dst, const void* src, size_t bytes, bool to_staging = fals
         const size_t a = bytes * k / t, b = bytes * (k + 1) / t;
         copy(static_cast<char*>(dst) + a, static_cast<const char*>(src) + a, b - a);
     };
-    for (size_t k = 1; k < t; ++k) th.emplace_back(part, k);
+    size_t k = 1;
+    try {  // no exception may leave the C ABI: pieces without a thread are copied here
+        for (; k < t; ++k) th.emplace_back(part, k);
+    } catch (...) {
+    }
+    for (size_t r = k; r < t; ++r) part(r);
     part(0);
     for (auto& x : th) x.join();
 }
