@@ -341,10 +341,10 @@ class ShardedAdmm:
             self._ev.append((e0, e1))
         if self.world > 1:  # consensus exchange: in-place all-gather of the branch solutions
             mine = self.x[self.rank * self.chunk:(self.rank + 1) * self.chunk]
-            dist.all_gather_into_tensor(self.x, mine)
+            self._all_gather(self.x, mine)
         self.solver.update_consensus(st, self.res.data_ptr())
         if self.world > 1:
-            dist.all_reduce(self.res, op=dist.ReduceOp.MAX)
+            self._all_reduce_max(self.res)
         p, d, bad = self.res.tolist()
         self.history.append((p, d))
         if bad >= 0:  # a failed branch solve propagates (from every rank)
@@ -353,6 +353,35 @@ class ShardedAdmm:
             st_ = int(self.solver.get(BRANCH_STATUS)[b]) if lo <= b < hi else -1
             raise SolverError(f"ADMM branch stage: branch {b} failed with status {st_}")
         return p, d
+
+    # NCCL moves the device buffers directly (the GPU path); other backends
+    # (gloo: several ranks sharing one GPU in the tests) go through host copies
+    # of the same bytes, so the trajectory is identical either way
+    def _nccl(self) -> bool:
+        import torch.distributed as dist
+
+        return dist.get_backend() == "nccl"
+
+    def _all_gather(self, out, mine):
+        import torch.distributed as dist
+
+        if self._nccl():
+            dist.all_gather_into_tensor(out, mine)
+            return
+        h = mine.cpu()
+        ho = self.torch.empty((out.shape[0],) + tuple(out.shape[1:]), dtype=out.dtype)
+        dist.all_gather_into_tensor(ho, h)
+        out.copy_(ho)
+
+    def _all_reduce_max(self, t):
+        import torch.distributed as dist
+
+        if self._nccl():
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            return
+        h = t.cpu()
+        dist.all_reduce(h, op=dist.ReduceOp.MAX)
+        t.copy_(h)
 
     def partition_times(self) -> List[List[float]]:
         """[iteration][rank] seconds of the branch stage of every recorded
@@ -364,6 +393,8 @@ class ShardedAdmm:
                                  device=self.dev)
         if self.world == 1:
             return [[t] for t in mine.tolist()]
+        if not self._nccl():
+            mine = mine.cpu()
         allt = [self.torch.empty_like(mine) for _ in range(self.world)]
         dist.all_gather(allt, mine)
         return [list(r) for r in zip(*[a.tolist() for a in allt])]
