@@ -329,6 +329,19 @@ int check_batch(const tb_problem_batch* b, int64_t* nparams) {
 
 constexpr int64_t kChunkMin = 4096;  // problems per chunk of the host-buffer pipeline
 
+// Debug builds only (-DTB_TRACE_HOST): host-side timeline of tb_solve_batch
+// on stderr; `sync` waits for the device first (perturbs the overlap).
+#ifdef TB_TRACE_HOST
+#define TB_TRACE(what, sync)                                                                                  \
+    do {                                                                                                     \
+        if (sync) cudaDeviceSynchronize();                                                                    \
+        fprintf(stderr, "[tb trace] %-22s %8.3f ms\n", what,                                                 \
+                std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count() * 1e3);         \
+    } while (0)
+#else
+#define TB_TRACE(what, sync)
+#endif
+
 // Copy into page-locked staging with non-temporal stores: a DMA that reads
 // lines the CPU just wrote (still dirty in its caches) runs at ~17 GB/s on
 // the B200 boxes, the same bytes written with streaming stores at the full
@@ -358,27 +371,37 @@ void stream_memcpy(void* dst, const void* src, size_t bytes) {
 }
 
 // Host copies between caller (pageable) memory and the pinned staging: one
-// thread moves ~17 GB/s, so copies of a few MB are split over host threads
-// (the staging of a ranked C2 batch is 28 MB in, 6 MB out); `to_staging`
-// selects the streaming stores.
-void par_memcpy(void* dst, const void* src, size_t bytes, bool to_staging = false) {
+// thread moves ~17 GB/s, so a set of copies of a few MB is split over host
+// threads started once for the whole set (the staging of a ranked C2 batch is
+// 28 MB in four arrays, 6 MB out in nine); `to_staging` selects the
+// streaming stores.
+struct HostCopy {
+    void* dst;
+    const void* src;
+    size_t bytes;
+};
+void par_memcpy_set(const HostCopy* jobs, int njobs, bool to_staging) {
     constexpr size_t kPiece = size_t(1) << 18;
+    size_t total = 0;
+    for (int j = 0; j < njobs; ++j) total += jobs[j].src && jobs[j].dst ? jobs[j].bytes : 0;
     const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
-    const size_t t = std::min<size_t>(std::min<size_t>(hw, 8), bytes / kPiece);
-    auto copy = [&](void* d, const void* s, size_t n) {
-        if (to_staging) stream_memcpy(d, s, n);
-        else std::memcpy(d, s, n);
+    const size_t t = std::max<size_t>(1, std::min<size_t>(std::min<size_t>(hw, 8), total / kPiece));
+    auto part = [&](size_t k) {  // slice k of every copy of the set
+        for (int j = 0; j < njobs; ++j) {
+            const HostCopy& c = jobs[j];
+            if (!c.src || !c.dst) continue;
+            const size_t a = c.bytes * k / t, b = c.bytes * (k + 1) / t;
+            if (b <= a) continue;
+            if (to_staging) stream_memcpy(static_cast<char*>(c.dst) + a, static_cast<const char*>(c.src) + a, b - a);
+            else std::memcpy(static_cast<char*>(c.dst) + a, static_cast<const char*>(c.src) + a, b - a);
+        }
     };
     if (t <= 1) {
-        copy(dst, src, bytes);
+        part(0);
         return;
     }
     std::vector<std::thread> th;
     th.reserve(t - 1);
-    auto part = [&](size_t k) {
-        const size_t a = bytes * k / t, b = bytes * (k + 1) / t;
-        copy(static_cast<char*>(dst) + a, static_cast<const char*>(src) + a, b - a);
-    };
     size_t k = 1;
     try {  // no exception may leave the C ABI: pieces without a thread are copied here
         for (; k < t; ++k) th.emplace_back(part, k);
@@ -782,10 +805,8 @@ static int solve_batch_impl(tb_context* ctx, const tb_problem_batch* b, const tb
                         cb->pack(cb->user, g0, g0 + cc, reinterpret_cast<double*>(hx), reinterpret_cast<double*>(hl),
                                  reinterpret_cast<double*>(hu), cpb ? reinterpret_cast<double*>(hp) : nullptr);
                     } else {
-                        par_memcpy(hx, x0, cvb, true);
-                        par_memcpy(hl, lw, cvb, true);
-                        par_memcpy(hu, up, cvb, true);
-                        if (cpb) par_memcpy(hp, prm, cpb, true);
+                        const HostCopy set[4] = {{hx, x0, cvb}, {hl, lw, cvb}, {hu, up, cvb}, {hp, prm, cpb}};
+                        par_memcpy_set(set, 4, true);
                     }
                     x0 = reinterpret_cast<const double*>(hx);
                     lw = reinterpret_cast<const double*>(hl);
@@ -850,6 +871,8 @@ static int solve_batch_impl(tb_context* ctx, const tb_problem_batch* b, const tb
             }
             if (!ranked) CUDA_TRY(cudaEventRecord(d.ev[2], d.stream));  // chunked: includes the last D2H
         }
+        TB_TRACE("inputs issued", false);
+        TB_TRACE("inputs on device", true);
         if (ranked) {
             tbdev::KernelArgs a = part_args();
             CUDA_TRY(attach_ws(d, b->family, a, d.stream));
@@ -859,6 +882,7 @@ static int solve_batch_impl(tb_context* ctx, const tb_problem_batch* b, const tb
             CUDA_TRY(release_order(d, a, d.stream));
             CUDA_TRY(release_ws(d, a, d.stream));
             CUDA_TRY(cudaEventRecord(d.ev[2], d.stream));
+            TB_TRACE("ranked solve done", true);
             if (out_host) {
                 auto tgt = [&](auto* user, auto* stage, int64_t m) -> decltype(user) {
                     if (!user && !(cb && stage)) return nullptr;  // callbacks: every report field
@@ -883,6 +907,8 @@ static int solve_batch_impl(tb_context* ctx, const tb_problem_batch* b, const tb
         CUDA_TRY(cudaEventRecord(d.ev[3], d.stream));
     }
 
+    TB_TRACE("all issued", false);
+    TB_TRACE("results on host", true);
     // pageable outputs: copy each chunk out of the pinned staging as soon as
     // it completes (later chunks keep solving meanwhile)
     if (out_host && !out_pinned) {
@@ -916,8 +942,10 @@ static int solve_batch_impl(tb_context* ctx, const tb_problem_batch* b, const tb
                     if (cc > 0) cb->unpack(cb->user, g0, g0 + cc, &v);
                     continue;
                 }
+                HostCopy set[9];
+                int nj = 0;
                 auto out = [&](auto* user, auto* stage, int64_t m) {
-                    if (user) par_memcpy(user + g0 * m, stage + a0 * m, sizeof(*user) * (size_t)(cc * m));
+                    if (user) set[nj++] = {user + g0 * m, stage + a0 * m, sizeof(*user) * (size_t)(cc * m)};
                 };
                 out(r->x_star, hst.x_star, n);
                 out(r->f_star, hst.f_star, 1);
@@ -928,9 +956,11 @@ static int solve_batch_impl(tb_context* ctx, const tb_problem_batch* b, const tb
                 out(r->f_evals, hst.fev, 1);
                 out(r->flops, hst.flops, 1);
                 out(r->wall_time, hst.wall, 1);
+                par_memcpy_set(set, nj, false);
             }
         }
     }
+    TB_TRACE("copied out", false);
     double kmax = 0.0;
     for (int k = 0; k < G; ++k) {
         DevState& d = ctx->devs[k];
