@@ -12,6 +12,10 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <condition_variable>
+#include <functional>
+#include <memory>
+#include <mutex>
 #include <string>
 #include <thread>
 #include <vector>
@@ -119,8 +123,76 @@ __global__ void first_error_kernel(const int32_t* status, long long count, unsig
 
 }  // namespace
 
+// Host threads of a context for its staging copies, started once (starting
+// threads for every copy set costs ~0.1 ms, as much as the copies they share).
+class HostPool {
+public:
+    explicit HostPool(int n) : nt_(n < 1 ? 1 : n) {
+        for (int k = 1; k < nt_; ++k) th_.emplace_back([this, k] { loop(k); });
+    }
+    ~HostPool() {
+        {
+            std::lock_guard<std::mutex> g(m_);
+            stop_ = true;
+            ++gen_;
+        }
+        cv_.notify_all();
+        for (auto& t : th_) t.join();
+    }
+    int size() const { return nt_; }
+    // fn(k) for k in [0, t), t <= size(); the caller runs k = 0
+    void run(int t, const std::function<void(int)>& fn) {
+        if (t <= 1) {
+            fn(0);
+            return;
+        }
+        {
+            std::lock_guard<std::mutex> g(m_);
+            job_ = &fn;
+            jobs_ = t;
+            pending_ = nt_ - 1;
+            ++gen_;
+        }
+        cv_.notify_all();
+        fn(0);
+        std::unique_lock<std::mutex> l(m_);
+        done_.wait(l, [&] { return pending_ == 0; });
+        job_ = nullptr;
+    }
+
+private:
+    void loop(int k) {
+        unsigned long long seen = 0;
+        for (;;) {
+            const std::function<void(int)>* job;
+            int jobs;
+            {
+                std::unique_lock<std::mutex> l(m_);
+                cv_.wait(l, [&] { return gen_ != seen; });
+                seen = gen_;
+                if (stop_) return;
+                job = job_;
+                jobs = jobs_;
+            }
+            if (k < jobs) (*job)(k);
+            std::lock_guard<std::mutex> g(m_);
+            if (--pending_ == 0) done_.notify_one();
+        }
+    }
+    int nt_;
+    std::vector<std::thread> th_;
+    std::mutex m_;
+    std::condition_variable cv_, done_;
+    const std::function<void(int)>* job_ = nullptr;
+    int jobs_ = 0;
+    int pending_ = 0;
+    unsigned long long gen_ = 0;
+    bool stop_ = false;
+};
+
 struct tb_context {
     std::vector<DevState> devs;
+    std::unique_ptr<HostPool> pool;  // staging copies (created on the first host-buffer solve)
     int mode = TB_MODE_EXACT;
     int fast_forward = 1;
     int form = TB_FORM_AUTO;
@@ -380,7 +452,7 @@ struct HostCopy {
     const void* src;
     size_t bytes;
 };
-void par_memcpy_set(const HostCopy* jobs, int njobs, bool to_staging) {
+void par_memcpy_set(HostPool* pool, const HostCopy* jobs, int njobs, bool to_staging) {
     constexpr size_t kPiece = size_t(1) << 18;
     size_t total = 0;
     for (int j = 0; j < njobs; ++j) total += jobs[j].src && jobs[j].dst ? jobs[j].bytes : 0;
@@ -398,6 +470,13 @@ void par_memcpy_set(const HostCopy* jobs, int njobs, bool to_staging) {
     };
     if (t <= 1) {
         part(0);
+        return;
+    }
+    if (pool) {
+        const int tp = (int)std::min<size_t>(t, (size_t)pool->size());
+        pool->run(tp, [&](int k) {
+            for (size_t r = (size_t)k; r < t; r += (size_t)tp) part(r);
+        });
         return;
     }
     std::vector<std::thread> th;
@@ -697,6 +776,12 @@ static int solve_batch_impl(tb_context* ctx, const tb_problem_batch* b, const tb
         !cb && (!out_host || (is_pinned(r->x_star) && is_pinned(r->f_star) && is_pinned(r->pg_norm) &&
                               is_pinned(r->status) && is_pinned(r->iterations) && is_pinned(r->cg_iterations) &&
                               is_pinned(r->f_evals) && is_pinned(r->wall_time) && is_pinned(r->flops)));
+    if (((in_host && !in_pinned) || (out_host && !out_pinned)) && !ctx->pool) {
+        try {  // host threads for the staging copies; without them the copies run serially
+            ctx->pool = std::make_unique<HostPool>((int)std::min(8u, std::max(1u, std::thread::hardware_concurrency())));
+        } catch (...) {
+        }
+    }
     int64_t first_bad = -1;  // first problem the reference would have thrown on (batch.hpp:75-76)
     int bad_status = 0;
     std::vector<int> nchs(G, 1);
@@ -713,10 +798,10 @@ static int solve_batch_impl(tb_context* ctx, const tb_problem_batch* b, const tb
         CUDA_TRY(tbdev::tron_ws_need(b->family, n, c, ctx->form, &ws_need));
         // Ranked partitions solve in ONE launch in rank order
         // once the whole partition is on the device (a problem's rank spans
-        // the partition), so their inputs go over in one piece (pageable ones
-        // through a multi-threaded host copy into the staging); only the
-        // callers' pack callbacks keep the chunks (packing chunk i+1 overlaps
-        // chunk i's transfer)
+        // the partition): page-locked inputs go over in one piece; pageable
+        // inputs and the callers' pack callbacks keep the chunks, so the host
+        // staging (context thread team, streaming stores) or packing of chunk
+        // i+1 overlaps chunk i's transfer
         bool ranked = false;
         if (staged) {
             tbdev::KernelArgs stub = make_args(b, np, cfg, ctx->fast_forward, ctx->form, nullptr, nullptr, nullptr,
@@ -725,7 +810,7 @@ static int solve_batch_impl(tb_context* ctx, const tb_problem_batch* b, const tb
             stub.route_count = c;
             ranked = want_order(b->family, stub, ctx->order) || ctx->order == TB_ORDER_CALLER;
         }
-        const int nch = (staged && ws_need == 0 && c >= 2 * kChunkMin && (!ranked || cb))
+        const int nch = (staged && ws_need == 0 && c >= 2 * kChunkMin && (!ranked || cb || in_stage))
                             ? (int)std::min<int64_t>(max_chunks(true), c / kChunkMin)
                             : 1;
         nchs[k] = nch;
@@ -806,7 +891,7 @@ static int solve_batch_impl(tb_context* ctx, const tb_problem_batch* b, const tb
                                  reinterpret_cast<double*>(hu), cpb ? reinterpret_cast<double*>(hp) : nullptr);
                     } else {
                         const HostCopy set[4] = {{hx, x0, cvb}, {hl, lw, cvb}, {hu, up, cvb}, {hp, prm, cpb}};
-                        par_memcpy_set(set, 4, true);
+                        par_memcpy_set(ctx->pool.get(), set, 4, true);
                     }
                     x0 = reinterpret_cast<const double*>(hx);
                     lw = reinterpret_cast<const double*>(hl);
@@ -956,7 +1041,7 @@ static int solve_batch_impl(tb_context* ctx, const tb_problem_batch* b, const tb
                 out(r->f_evals, hst.fev, 1);
                 out(r->flops, hst.flops, 1);
                 out(r->wall_time, hst.wall, 1);
-                par_memcpy_set(set, nj, false);
+                par_memcpy_set(ctx->pool.get(), set, nj, false);
             }
         }
     }
