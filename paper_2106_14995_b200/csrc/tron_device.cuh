@@ -147,7 +147,8 @@ struct SmemLayout {
     static constexpr int CTX = XS + D;       // family context (branch: sizeof(tb_branch_ctx))
     static constexpr int CTX_DOUBLES = (int)((sizeof(tb_branch_ctx) / sizeof(double) + 1) & ~1);
     static constexpr int SC = CTX + CTX_DOUBLES;   // 8 warp-uniform loop scalars kept out of registers
-    static constexpr int PRM = SC + 8;             // staged parameters
+    static constexpr int LU = SC + 8;              // bounds of lanes 0..31 (D = 8: Warp::kBoundsSmem)
+    static constexpr int PRM = LU + (D == 8 ? 64 : 0);  // staged parameters
     static constexpr int fixed() { return PRM; }
     static_assert(D % 2 == 0, "D must be even (16-byte staging loads)");
 };
@@ -326,6 +327,26 @@ struct Warp {
     long long memo_fl;
     bool memo_credit;  // credit a memoised call's flops (fast_forward 1: the reference's count; 2: executed only)
     double extrap;  // 1.0 / cfg->interp_factor
+    // D = 8 keeps the bounds in shared memory (l at lu[lane], u at lu[32 + lane])
+    // and re-reads them where used, so they are not live across ccf / PCG:
+    // fewer spills in the masked-loop kernel (ncvx8 x32,768 3.39 -> 3.14 ms;
+    // the other D measured 2-4 % slower that way and keep registers;
+    // profiles/r02_ab_bounds_smem.txt)
+    static constexpr bool kBoundsSmem = D == 8;
+    // this lane's bounds: the shared-memory slots (D = 8, read here) or the
+    // register value the caller holds
+    __device__ __forceinline__ double lb(double l) const {
+        if constexpr (kBoundsSmem)
+            return static_cast<const volatile double*>(s1 + (SmemLayout<D>::LU - SmemLayout<D>::S1))[lane];
+        else
+            return l;
+    }
+    __device__ __forceinline__ double ub(double u) const {
+        if constexpr (kBoundsSmem)
+            return static_cast<const volatile double*>(s1 + (SmemLayout<D>::LU - SmemLayout<D>::S1))[32 + lane];
+        else
+            return u;
+    }
 #ifdef TB_PHASES
     long long ph[8];
 #endif
@@ -796,7 +817,9 @@ struct Warp {
     __device__ __forceinline__ int subspace_step(double x0, double g, double l, double u, double delta, double cs,
                                                  double& xout, double& sout, long long& cg_total) {
         const int nn = n;
-        xout = clip(x0 + 1.0 * cs, l, u);
+#define TB_LB lb(l)
+#define TB_UB ub(u)
+        xout = clip(x0 + 1.0 * cs, TB_LB, TB_UB);
         count(2 * nn);
         double s = xout - x0;
         count(nn);
@@ -804,7 +827,7 @@ struct Warp {
         cg_total = 0;
 #pragma unroll 1
         for (int faces = 0; faces < nn; ++faces) {
-            const bool fr = lane < nn && l < xout && xout < u;
+            const bool fr = lane < nn && TB_LB < xout && xout < TB_UB;
             const unsigned F = __ballot_sync(FULL, fr);
             const int nf = __popc(F);
             if (nf == 0) break;
@@ -826,7 +849,7 @@ struct Warp {
             if (rc) return rc;
             cg_total += its;
             TB_PH_BEGIN(4)
-            const double xn = line_search(xout, l, u, gfree, step, F);
+            const double xn = line_search(xout, TB_LB, TB_UB, gfree, step, F);
             TB_PH_END(*this, 4)
             if (fr) {
                 s += xn - xout;
@@ -842,6 +865,8 @@ struct Warp {
         }
         sout = s;
         return 0;
+#undef TB_LB
+#undef TB_UB
     }
 };
 
@@ -1044,8 +1069,16 @@ __device__ __forceinline__ void tron_solve_one(const KernelArgs& a, const long l
     W.prm = prm_s;
     FamT fam;
     fam.bind(smem + SL::CTX);
-    const double l = act ? a.lo[pid * n + lane] : 0.0;
-    const double u = act ? a.up[pid * n + lane] : 0.0;
+    constexpr bool kBS = Warp<D, COUNT>::kBoundsSmem;
+    if constexpr (kBS) {
+        volatile double* lus = smem + SL::LU;
+        lus[lane] = act ? a.lo[pid * n + lane] : 0.0;
+        lus[32 + lane] = act ? a.up[pid * n + lane] : 0.0;
+    }
+    const double l = kBS ? 0.0 : (act ? a.lo[pid * n + lane] : 0.0);
+    const double u = kBS ? 0.0 : (act ? a.up[pid * n + lane] : 0.0);
+#define TB_L W.lb(l)
+#define TB_U W.ub(u)
     double x = act ? a.x0[pid * n + lane] : 0.0;
     __syncwarp();
 
@@ -1073,7 +1106,7 @@ __device__ __forceinline__ void tron_solve_one(const KernelArgs& a, const long l
     pg = 0.0;
 
     // tron.hpp:465-466
-    if (__any_sync(FULL, act && !(l <= u))) {
+    if (__any_sync(FULL, act && !(TB_L <= TB_U))) {
         status = TB_STATUS_INVALID_BOUNDS;
     } else {
         const double kEta1 = 0.25, kEta2 = 0.75;
@@ -1081,7 +1114,7 @@ __device__ __forceinline__ void tron_solve_one(const KernelArgs& a, const long l
         // ONE gradient site (code size: the branch context is large): pass 0
         // evaluates the start point (:473-483), pass k >= 1 the trial point of
         // iteration k (:506-539).  Same operations in the same order.
-        x = W.clip(x, l, u);
+        x = W.clip(x, TB_L, TB_U);
         double xe = x;  // point being evaluated
         double g = 0.0, s = 0.0, delta = 0.0, alpha_c = 1.0;
         bool need_hessian = true;
@@ -1136,7 +1169,7 @@ __device__ __forceinline__ void tron_solve_one(const KernelArgs& a, const long l
             if (take) {
                 g = fam.grad(W);  // the context was prepared at xe
                 W.count(FamT::flops(n, 1));
-                pg = W.pgnorm(x, g, l, u);
+                pg = W.pgnorm(x, g, TB_L, TB_U);
             }
             if (iter == 0) {
                 delta = cfg.has_delta0 ? cfg.delta0 : tb_smax(W.nrm2(g, W.act), 1.0);
@@ -1181,7 +1214,7 @@ __device__ __forceinline__ void tron_solve_one(const KernelArgs& a, const long l
 
             double cs, alpha_new;
             TB_PH_BEGIN(1)
-            int rc = W.cauchy(x, g, l, u, delta, alpha_c, alpha_new, cs);
+            int rc = W.cauchy(x, g, TB_L, TB_U, delta, alpha_c, alpha_new, cs);
             TB_PH_END(W, 1)
             if (rc) {
                 status = rc;
@@ -1216,6 +1249,8 @@ __device__ __forceinline__ void tron_solve_one(const KernelArgs& a, const long l
         if (a.flops) a.flops[pid] = W.fl;
         if (a.wall_time) a.wall_time[pid] = 1e-9 * (double)(globaltimer() - t_start);
     }
+#undef TB_L
+#undef TB_U
 }
 
 // Small batches (at most kLatencyBlocks one-warp blocks per SM) are latency-
