@@ -55,6 +55,14 @@ constexpr int kThreadBlock = 64;
 #define TB_ADMM_ORDER 1
 #endif
 bool admm_ranked(long long cnt) { return TB_ADMM_ORDER && cnt > 4LL * kThreadBlock * tbdev::device_sm_count(); }
+// The fused augmented-Lagrangian stage (dim 6, one warp per branch) is ranked
+// like C2 beyond one wave of warps (profiles/r02_ab_admm_order.txt).
+#ifndef TB_ADMM_AL_ORDER
+#define TB_ADMM_AL_ORDER 1
+#endif
+bool admm_al_ranked(long long cnt) {
+    return TB_ADMM_AL_ORDER && cnt > (long long)tbdev::WarpMinBlocks<6>::value * tbdev::device_sm_count();
+}
 #ifndef TB_ADMM_BRANCH_MINB
 #define TB_ADMM_BRANCH_MINB 1  // resident 64-thread blocks per SM the register budget must allow
 #endif
@@ -279,13 +287,15 @@ __global__ void admm_cost_kernel(tb_admm_view v, double* out) {
 // branch of a round.  x is solved in place (each solve reads x0 before it
 // writes x*).  round_max receives the largest per-branch round count (= the
 // number of synchronous rounds the oracle runs).
+template <bool ORD>
 __global__ void __launch_bounds__(32, tbdev::WarpMinBlocks<6>::value)
     admm_auglag_fused_kernel(const __grid_constant__ tbdev::KernelArgs a, double* prm_shard, double* eta_shard,
                              double xi0, double eta0, double feas_tol, double xi_max, int max_rounds,
                              int* round_max) {
     extern __shared__ double smem[];
-    const long long pid = blockIdx.x;
-    if (pid >= a.count || stopped(a.skip)) return;
+    const long long k = blockIdx.x;
+    if (k >= a.count || stopped(a.skip)) return;
+    const long long pid = ORD ? (long long)a.order[k] : k;  // ORD: ranked launch (tron_order.cu)
     const int lane = threadIdx.x & 31;
     double* prm = prm_shard + pid * TB_BR_NPARAMS;
     if (lane == 0) {
@@ -528,7 +538,8 @@ int tb_admm_create(const tb_admm_grid* gr, const tb_admm_options* opt, int32_t d
         a->upper = dalloc<double>(a, (size_t)nl * D, &err);
         if (err == cudaSuccess) err = upload<double>(a->upper, hs.br_upper, (size_t)nl * D);
         a->status = dalloc<int32_t>(a, (size_t)nl, &err);
-        if (D == 4 && admm_ranked(nl)) a->ord = dalloc<char>(a, tbdev::order_ws_bytes(nl), &err);
+        if ((D == 4 && admm_ranked(nl)) || (D == 6 && admm_al_ranked(nl)))
+            a->ord = dalloc<char>(a, tbdev::order_ws_bytes(nl), &err);
         a->res = dalloc<unsigned long long>(a, 3, &err);
         a->cost = dalloc<double>(a, 1, &err);
         a->stop = dalloc<int>(a, 2, &err);
@@ -619,7 +630,12 @@ int enqueue_components(tb_admm* a, cudaStream_t st, const int* stop) {
         // (a thread-per-branch form of this loop measured 184 vs 283 iter/s on C4: the AL
         // rounds make the stage throughput-bound, where the warp form wins)
         const size_t smem = sizeof(double) * (size_t)(tbdev::SmemLayout<6>::fixed() + TB_BR_NPARAMS);
-        admm_auglag_fused_kernel<<<(unsigned)cnt, 32, smem, st>>>(
+        if (a->ord && admm_al_ranked(cnt)) {
+            const cudaError_t e = tbdev::launch_order(TB_FAMILY_BRANCH, k, a->ord, st, &k.order);
+            if (e != cudaSuccess) return fail(TB_E_CUDA, cudaGetErrorString(e));
+        }
+        auto al = k.order ? admm_auglag_fused_kernel<true> : admm_auglag_fused_kernel<false>;
+        al<<<(unsigned)cnt, 32, smem, st>>>(
             k, a->v.br_params + a->br_lo * TB_BR_NPARAMS, a->eta + a->br_lo, a->opt.auglag_xi0, a->opt.auglag_eta0,
             a->opt.auglag_feas_tol, a->opt.auglag_xi_max, a->opt.auglag_max_iter, a->round_max);
         admm_round_accum_kernel<<<1, 1, 0, st>>>(a->round_max, a->rounds_total, stop);
