@@ -2,10 +2,12 @@
 //
 // A one-shot launch ends with its slowest problem, and a problem that starts
 // late in the launch (blocks are dispatched in index order) finishes late.
-// The number of TRON iterations a problem needs is predicted well by the
-// projected-gradient inf-norm at its clipped start point -- the quantity
-// solve() tests first (tron.hpp:473-483): on C2 every problem that needs >=
-// 100 iterations is in the top quarter of that ranking.  So
+// For the branch family the number of TRON iterations a problem needs is
+// predicted well by the projected-gradient inf-norm at its clipped start
+// point -- the quantity solve() tests first (tron.hpp:473-483): on C2 every
+// problem that needs >= 100 iterations is in the top quarter of that ranking,
+// and the ranked launch runs as fast as one sorted by the oracle's actual
+// iteration counts (the host decides where ranking pays).  So
 // the library ranks the batch by it on the device and launches problem
 // order[k] as the k-th block / thread / work item.  Results are per problem
 // and written at the problem's own index: the order changes WHEN a problem
