@@ -145,7 +145,9 @@ int64_t tb_family_nparams(int32_t family, int32_t dim);
 /* Device context: one CUDA stream + reusable workspace per device.  The
  * reference's `workers` argument (batch.hpp:29) becomes the device list: the
  * batch is split in contiguous even partitions in input order over devices
- * (batch.hpp:61-70). */
+ * (batch.hpp:61-70).  A context (its staging buffers, workspaces and host
+ * thread team) serves one host thread at a time; use one context per host
+ * thread that solves concurrently. */
 int tb_context_create(const int32_t* devices, int32_t n_devices, tb_context** out);
 int tb_context_destroy(tb_context* ctx);
 /* mode must be TB_MODE_EXACT.  fast_forward: 1 (default) skips the provably
