@@ -730,6 +730,8 @@ def main():
             "cpu_baseline": cpu,
             "clocks": clocks.summary(),
             "gpu_launches": int(launches),
+            "launch_order": "ranked on the device by start projected-gradient norm (DESIGN.md 4g), inside the "
+                            "timed region: 3 order kernels + 1 solve launch per step",
             "parity": parity,
             "status_counts": {str(k): int(v) for k, v in zip(*np.unique(status, return_counts=True))},
             "admm_detail": sig(admm_line),
