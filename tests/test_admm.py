@@ -1,6 +1,8 @@
 """ADMM AC-OPF: the spec's closed-form examples, bus-update
 exactness against an independent KKT-QP oracle, the 2-bus toy against a full
 NLP solve, and (GPU) the device pipeline against the CPU oracle bit-for-bit."""
+import os
+
 import numpy as np
 import pytest
 
@@ -371,3 +373,22 @@ def test_device_admm_c4_matches_independent_restatement():
         worst = max(worst, r)
         assert r <= 1e-6, (k, r)
     print(f"C4 device vs independent restatement: max relative residual difference {worst:.2e}")
+
+
+@pytest.mark.gpu
+def test_ranked_line_limit_stage_bitwise_vs_oracle():
+    """Beyond one wave of warps the fused augmented-Lagrangian stage is
+    launched in rank order (start projected gradient); the
+    trajectory and the state stay the oracle's bit for bit."""
+    g = synth.grid(4200, 6300, 1260, seed=21, shunt_frac=0.3, rate=(0.05, 0.6))
+    opts = A.AdmmOptions(line_limits=True)
+    dev = A.AdmmSolver(g, opts)
+    cpu = po.OracleAdmm(g, opts, workers=os.cpu_count() or 8)
+    try:
+        for k in range(4):
+            assert dev.step() == cpu.step(), f"iteration {k}"
+        for what in (A.BRANCH_X, A.BRANCH_PARAMS, A.AUGLAG_ROUNDS, A.LINE_VIOL, A.BUS_WT):
+            assert np.array_equal(dev.get(what), cpu.get(what)), what
+    finally:
+        dev.close()
+        cpu.close()
