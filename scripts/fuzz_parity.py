@@ -21,7 +21,8 @@ while time.time() < t_end:
     fam = rng.choice(["ncvx", "boxqp", "hs45", "branch"], p=[0.45, 0.3, 0.1, 0.15])
     if fam == "branch":
         d = int(rng.choice([4, 6]))
-        n = int(rng.integers(1, 3000))
+        # FUZZ_BIG=1: also batches past one wave (AUTO ranks them; the d = 4 thread form from 16,384)
+        n = int(rng.integers(1, 3000 if not os.environ.get("FUZZ_BIG") or rng.random() < 0.7 else 24000))
     else:
         d = int(rng.choice([rng.integers(1, 21), rng.integers(21, 65), rng.integers(65, 129)], p=[0.6, 0.3, 0.1]))
         n = int(rng.integers(1, 400 if d <= 20 else (48 if d <= 64 else 8)))
