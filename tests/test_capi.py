@@ -91,3 +91,15 @@ def test_solver_fails_loudly_without_gpu():
 
     with pytest.raises(SolverError):
         Solver((0,))
+
+
+def test_python_enums_match_the_header():
+    """KernelForm / LaunchOrder mirror the header's TB_FORM_* / TB_ORDER_*."""
+    from paper_2106_14995_b200 import KernelForm, LaunchOrder
+
+    src = open(os.path.join(ROOT, "include", "tb_capi.h")).read()
+    defs = {k: int(v) for k, v in re.findall(r"#define\s+(TB_(?:FORM|ORDER)_[A-Z_]+)\s+(\d+)", src)}
+    forms = {k[len("TB_FORM_"):]: v for k, v in defs.items() if k.startswith("TB_FORM_")}
+    orders = {k[len("TB_ORDER_"):]: v for k, v in defs.items() if k.startswith("TB_ORDER_")}
+    assert forms == {m.name: int(m) for m in KernelForm}
+    assert orders == {m.name: int(m) for m in LaunchOrder}
