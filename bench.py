@@ -666,7 +666,9 @@ def main():
             os.remove(path)
             dropin = json.loads(out.stdout.strip().splitlines()[-1])
             dropin["note"] = ("C++ drop-in tronbatch::gpu::solve_batch end to end: vector<BranchProblem> packing, "
-                              "pinned staging, pipeline, 65,536 SolveReports (tests/cpp/gpu_dropin_bench.cpp)")
+                              "pinned staging, pipeline, 65,536 SolveReports (tests/cpp/gpu_dropin_bench.cpp); "
+                              "value_incl_freeing_previous_result also times destroying the caller's previous "
+                              "BatchResult (65,536 heap vectors) in `br = solve_batch(...)`")
         except Exception as e:
             dropin = {"value": None, "error": repr(e)}
 
