@@ -42,6 +42,22 @@ def test_c5_grid_admm_bitwise_vs_oracle():
         assert np.array_equal(dev.solver.get(what), cpu.get(what)), what
 
 
+def test_c5_graph_run_with_ranked_stage_equals_steps():
+    """C5's branch stage is ranked (beyond one wave); the order
+    kernels are captured in tb_admm_run's CUDA graph.  The graph run and the
+    blocking steps (bitwise = the oracle, above) must leave the same state."""
+    g = c5_grid()
+    a, b = A.AdmmSolver(g), A.AdmmSolver(g)
+    try:
+        steps = [a.step() for _ in range(4)]
+        assert list(b.run(4, check_every=2)) == steps  # residual trajectory, bit for bit
+        for what in STATE:
+            assert np.array_equal(a.get(what), b.get(what)), what
+    finally:
+        a.close()
+        b.close()
+
+
 def test_multi_partition_context_on_one_gpu():
     """tb_solve_batch over a context of devices (0, 0): two partitions, each on
     its own stream, bit-identical to one partition; two partition times."""
