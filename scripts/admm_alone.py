@@ -1,3 +1,5 @@
+"""The C4 branch-stage batch after 30 ADMM iterations, solved alone (device-resident) for timing /
+captures of the stage without the rest of the iteration."""
 import os, sys
 sys.path.insert(0, '.')
 import numpy as np, torch

@@ -1,3 +1,4 @@
+"""Quick host-buffer timing of a few shapes with flop counts (solves/s and TFLOP/s per shape)."""
 import sys, time, numpy as np, torch
 sys.path.insert(0, ".")
 from paper_2106_14995_b200 import Solver, TronConfig, synth

@@ -1,3 +1,5 @@
+"""Host timeline of C2 with pageable buffers: run under a TB_TRACE_HOST build (TB_LIB_PATH=...)
+to print the staging / transfer / solve / copy-out marks of tb_solve_batch."""
 import sys, time; sys.path.insert(0,'.')
 import numpy as np
 from paper_2106_14995_b200 import Solver, synth
